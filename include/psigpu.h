@@ -1,0 +1,255 @@
+/*
+ * psigpu.h — C-ABI of the B200 (sm_100a) imaginary-time FDTD hot path.
+ *
+ * This is the drop-in boundary for the hot path of the reference package
+ * `psibox` (/root/reference/pkg/src/psibox).  Plain pointers, sizes and int
+ * status codes only; no torch or CUDA types appear in the signatures
+ * (streams and device pointers travel as `void*` / `double*`).
+ *
+ * Two layers:
+ *
+ *  1. Operator layer (psg_kernel_*): one entry point per numba kernel of
+ *     kernels.py.  Same argument meaning as the reference (host numpy
+ *     arrays of shape (planes, ext, ext), C order, inclusive local plane
+ *     range x_lo..x_hi, outputs written into caller-supplied arrays,
+ *     padding never written).  Each call uploads, runs the CUDA kernel and
+ *     downloads; it is the literal replacement a ctypes binding of
+ *     `psibox.kernels` would make.
+ *
+ *  2. Engine layer (psg_*): a device-resident slab (one GPU, local planes
+ *     0..W+1 of a lattice of N^3 interior sites) that keeps psi, V and the
+ *     reduction scratch in HBM and runs sweeps, fused norm/observable
+ *     reductions, parity imposition and trilinear resampling without
+ *     host round trips.  It replaces the per-sweep body of
+ *     evolve.SweepBuffers / evolve_to_convergence (evolve.py:160-272) and of
+ *     parallel._worker_loop (parallel.py:393-506).
+ *
+ * Status codes map onto psibox.errors (errors.py:1-45) in the Python host:
+ *   PSG_OK               0
+ *   PSG_ERR_CONFIG       1  -> ConfigError
+ *   PSG_ERR_CUDA         2  -> RuntimeError (CUDA failure; message in psg_last_error)
+ *   PSG_ERR_ZERO_NORM    3  -> ZeroNormError
+ *   PSG_ERR_DIVERGED     4  -> DivergenceError
+ *   PSG_ERR_SINGULAR     5  -> SingularCoefficientError
+ *   PSG_ERR_NO_DEVICE    6  -> RuntimeError (no CUDA device: there is no CPU fallback)
+ */
+#ifndef PSIGPU_H
+#define PSIGPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PSG_OK 0
+#define PSG_ERR_CONFIG 1
+#define PSG_ERR_CUDA 2
+#define PSG_ERR_ZERO_NORM 3
+#define PSG_ERR_DIVERGED 4
+#define PSG_ERR_SINGULAR 5
+#define PSG_ERR_NO_DEVICE 6
+
+/* sweep / reduction flags */
+#define PSG_F_WRITE 1u   /* update psi (stencil_update) */
+#define PSG_F_NORM 2u    /* per-plane sum of out^2 (norm_plane_sums on the output) */
+#define PSG_F_MEASURE 4u /* per-plane num/den/r2 on the input (energy_ + radius2_plane_sums) */
+
+/* reduction quantity slots in the plane-sum vectors */
+#define PSG_Q_NUM 0
+#define PSG_Q_DEN 1
+#define PSG_Q_R2 2
+#define PSG_Q_NORM 3
+
+/* ------------------------------------------------------------------ */
+/* misc                                                                 */
+/* ------------------------------------------------------------------ */
+
+/* ABI version of this header (bumped on any signature change). */
+int psg_abi_version(void);
+/* Thread-local message of the last failing call ("" when none). */
+const char* psg_last_error(void);
+/* Number of visible CUDA devices (0 on a machine without a GPU). */
+int psg_device_count(void);
+
+/* Device layout of a slab: [planes][ext][pitch] doubles, column of site k
+ * at k + 3 so that interior rows start 32-byte aligned.  Returns the row
+ * pitch (doubles) for a lattice of n interior sites per axis. */
+int64_t psg_row_pitch(int64_t n);
+
+/* numpy.sum replica (pairwise, 8 accumulators, 128 blocks) on the device:
+ * replaces observables.combine_plane_sums (observables.py:32-34) where the
+ * combine must happen without a host round trip.  out[0] = sum(a[0..n)). */
+int psg_pairwise_sum_device(const double* host_a, int64_t n, double* out);
+
+/* ------------------------------------------------------------------ */
+/* 1. operator layer: kernels.py entry points on host arrays             */
+/* ------------------------------------------------------------------ */
+
+/* kernels.stencil_update(psi, coef_a, coef_c, out, x_lo, x_hi)  kernels.py:22-37
+ * arrays are (planes, ext, ext) C-order fp64, ext = N+2. */
+int psg_kernel_stencil_update(const double* psi, const double* coef_a, const double* coef_c,
+                              double* out, int64_t planes, int64_t ext, int64_t x_lo,
+                              int64_t x_hi);
+
+/* Same update with A and C synthesised from V in-kernel (potential._coefficients
+ * order, potential.py:102-115): 24 B/site instead of 32. */
+int psg_kernel_stencil_update_v(const double* psi, const double* v, double dtau, double m,
+                                double a, double* out, int64_t planes, int64_t ext,
+                                int64_t x_lo, int64_t x_hi);
+
+/* kernels.norm_plane_sums(psi, x_lo, x_hi, out)  kernels.py:40-49 */
+int psg_kernel_norm_plane_sums(const double* psi, int64_t planes, int64_t ext, int64_t x_lo,
+                               int64_t x_hi, double* out);
+
+/* kernels.energy_plane_sums(psi, v, kin, x_lo, x_hi, num_out, den_out)  kernels.py:52-74 */
+int psg_kernel_energy_plane_sums(const double* psi, const double* v, double kin, int64_t planes,
+                                 int64_t ext, int64_t x_lo, int64_t x_hi, double* num_out,
+                                 double* den_out);
+
+/* kernels.radius2_plane_sums(psi, x_global0, center, a, x_lo, x_hi, r2_out, den_out)
+ * kernels.py:77-100 */
+int psg_kernel_radius2_plane_sums(const double* psi, int64_t x_global0, double center, double a,
+                                  int64_t planes, int64_t ext, int64_t x_lo, int64_t x_hi,
+                                  double* r2_out, double* den_out);
+
+/* kernels.dot_plane_sums(psi1, psi2, x_lo, x_hi, out)  kernels.py:103-112 */
+int psg_kernel_dot_plane_sums(const double* psi1, const double* psi2, int64_t planes,
+                              int64_t ext, int64_t x_lo, int64_t x_hi, double* out);
+
+/* ------------------------------------------------------------------ */
+/* 2. engine layer: device-resident slab                                 */
+/* ------------------------------------------------------------------ */
+
+typedef struct psg_slab psg_slab;
+
+/* Create a slab on `device` for a lattice (N=n, a, m, dtau) owning the
+ * global interior planes x_lo..x_lo+w-1 (1-based; w=n for one GPU).
+ * Allocates psi (2 buffers), V and reduction scratch in HBM, all zeroed
+ * (Dirichlet padding).  Mirrors evolve.SweepBuffers (evolve.py:160-166)
+ * and parallel.Worker (parallel.py:125-176). */
+int psg_create(int device, int64_t n, int64_t w, int64_t x_lo, double a, double m, double dtau,
+               psg_slab** out);
+int psg_destroy(psg_slab* s);
+
+/* The slab's CUDA stream (cudaStream_t as void*). */
+void* psg_stream(psg_slab* s);
+int psg_sync(psg_slab* s);
+
+/* Geometry: pitch (doubles per row), plane stride (doubles), local planes (w+2). */
+int psg_geometry(psg_slab* s, int64_t* pitch, int64_t* plane_stride, int64_t* planes);
+
+/* Device pointer of local plane `p` (0..w+1) of the current psi buffer
+ * (which=0) or the other buffer (which=1); plane is `plane_stride`
+ * contiguous doubles.  Used by the host for halo exchange (NCCL). */
+double* psg_plane_ptr(psg_slab* s, int which, int64_t p);
+
+/* Upload `count` planes of a dense host field (ext x ext doubles each,
+ * C order) into local planes first..first+count-1 of BOTH psi buffers and
+ * reset the pending normalisation scale to 1.  Padding rows/cols are
+ * copied as given (evolve.step carries padding over, evolve.py:45-53). */
+int psg_set_field(psg_slab* s, const double* host, int64_t first, int64_t count);
+
+/* Download local planes first..first+count-1 of the current state,
+ * materialised (pending normalisation applied, exactly psi *= f of
+ * evolve.py:180). */
+int psg_get_field(psg_slab* s, double* host, int64_t first, int64_t count);
+
+/* Upload the potential for local planes first..first+count-1 (dense host
+ * planes, ext x ext).  Returns PSG_ERR_SINGULAR and the offending global
+ * site in bad_site[3] when 1 + (dtau/2) V == 0 (potential.py:103-110). */
+int psg_set_potential(psg_slab* s, const double* host_v, int64_t first, int64_t count,
+                      int64_t* bad_site);
+
+/* Use streamed A/C coefficient arrays (psibox PotentialGrid.coef_a/coef_c)
+ * instead of synthesising them from V (32 B/site path, kernels.py:37). */
+int psg_set_coefficients(psg_slab* s, const double* host_a, const double* host_c, int64_t first,
+                         int64_t count);
+
+/* One sweep of local planes z_lo..z_hi (inclusive) from the current buffer
+ * into the other one, with the fused reductions selected by flags
+ * (PSG_F_WRITE | PSG_F_NORM | PSG_F_MEASURE).  Does not swap. */
+int psg_sweep(psg_slab* s, int64_t z_lo, int64_t z_hi, unsigned flags);
+
+/* Swap current/other buffers (SweepBuffers.sweep's swap, evolve.py:169).
+ * `renorm`: the sweep just finished carried PSG_F_NORM and the next state
+ * must be read through the factor produced by psg_reduce. */
+int psg_swap(psg_slab* s, int renorm);
+
+/* Reduce the tile partials of the last sweep (or psg_measure) for local
+ * planes z_lo..z_hi into the global plane-sum vectors (slots PSG_Q_*, each
+ * n doubles, zero outside the slab).  combine != 0 also runs the numpy
+ * pairwise combine on the device and produces the scalars (totals, E,
+ * norm2, r_rms, next normalisation factor). */
+int psg_reduce(psg_slab* s, int64_t z_lo, int64_t z_hi, unsigned flags, int combine);
+
+/* Device pointer of the plane-sum vectors [4][n] (for an all-reduce of
+ * the zero-padded vectors across slabs). */
+double* psg_plane_sums_ptr(psg_slab* s);
+
+/* Combine only (after an external all-reduce of the plane sums). */
+int psg_combine(psg_slab* s, unsigned flags);
+
+/* Copy the plane sums [4][n] and the scalars to the host:
+ * scal[0..3] = totals (num, den, r2, norm), scal[4] = E, scal[5] = norm2
+ * (den*a^3), scal[6] = r_rms, scal[7] = n2 (norm*a^3), scal[8] = next
+ * factor 1/sqrt(n2), scal[9] = status (0 ok, 3 zero norm, 4 non-finite). */
+int psg_read_sums(psg_slab* s, double* plane_sums, double* scal);
+
+/* Observables of the current state without updating it (energy_plane_sums +
+ * radius2_plane_sums, observables.py:73-97), leaves partials for psg_reduce. */
+int psg_measure(psg_slab* s, int64_t z_lo, int64_t z_hi);
+
+/* Dot-product partials of the current state with a second slab's current
+ * state (dot_plane_sums, kernels.py:103-112), into PSG_Q_NUM. */
+int psg_dot(psg_slab* s, psg_slab* other, int64_t z_lo, int64_t z_hi);
+
+/* Apply the pending normalisation to the stored state (psi *= f). */
+int psg_materialize(psg_slab* s);
+
+/* Scale the stored state by an explicit factor (renormalize(), evolve.py:56-64). */
+int psg_scale(psg_slab* s, double factor);
+
+/* Reflection-parity imposition on a slab that holds the whole lattice
+ * (w == n): mode 0 = copy (states.impose_inplace, states.py:70-82),
+ * mode 1 = projector psi <- (psi + sign * R psi) * 0.5.  axis 0/1/2 is the
+ * storage axis, sign = +1 / -1.  The pending scale is applied on the fly. */
+int psg_impose(psg_slab* s, int axis, int sign, int mode);
+
+/* Trilinear resampling (multires.resample, multires.py:116-154) of the
+ * coarse slab's state into the fine slab's interior: per-axis coarse
+ * padded indices i0 (lo = i0, hi = i0+1) and fractions for each fine site
+ * (length fine n), computed by the host exactly as multires does.  The
+ * fine slab must hold the whole fine lattice.  No renormalisation. */
+int psg_resample(psg_slab* coarse, psg_slab* fine, const int64_t* i0, const double* frac);
+
+/* Run parameters of the fused fixed-step driver (one GPU, w == n). */
+typedef struct psg_run_params {
+  int64_t steps;          /* sweeps to run */
+  int64_t measure_every;  /* observables on the state entering sweep s when (s-1) % m == 0, s>1; 0 = never */
+  int64_t norm_every;     /* renormalise after sweep s when s % k == 0; 0 = never */
+  int64_t reimpose_every; /* impose after sweep s when s % r == 0; 0 = never */
+  int32_t impose_axis;    /* storage axis of the constraint */
+  int32_t impose_sign;    /* +1 / -1 */
+  int64_t step_offset;    /* index of the first sweep minus one (for resumed runs) */
+} psg_run_params;
+
+/* Fused fixed-step driver: runs the evolve_to_convergence loop body
+ * (evolve.py:249-270) for `steps` sweeps without host round trips.
+ * Measurement records go to hist (host, may be NULL): per check c,
+ * hist[c*(3n+2)+0..] = step index, status, then 3n plane sums
+ * (num | den | r2).  max_checks bounds the history. */
+int psg_run(psg_slab* s, const psg_run_params* p, double* hist, int64_t max_checks,
+            int64_t* n_checks);
+
+/* Kernel tuning knobs (0 = keep): blocks per SM for the sweep, z chunk. */
+int psg_tune(psg_slab* s, int blocks_per_sm, int zchunk);
+
+/* Number of kernels this slab has launched so far. */
+int64_t psg_launch_count(psg_slab* s);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PSIGPU_H */

@@ -1,0 +1,192 @@
+"""Device-resident slab: the Python face of the psg_* engine (include/psigpu.h).
+
+A :class:`Slab` owns one GPU's share of the lattice in HBM: two psi buffers
+(ping-pong, evolve.SweepBuffers, evolve.py:160-181), V, and the reduction
+scratch.  Whole-lattice runs use one slab with w == N; the slab engine of
+:mod:`paper_0904_0939_b200.parallel` uses one slab per GPU (w = N/M).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from ._lib import F_MEASURE, F_NORM, F_WRITE, NSCAL, RunParams, check, dptr, lptr
+from .errors import ConfigError, DeviceError, SingularCoefficientError
+from .lattice import LatticeSpec
+
+__all__ = ["Slab", "F_WRITE", "F_NORM", "F_MEASURE"]
+
+
+class Slab:
+    """One GPU's slab of local planes 0..w+1 (global x_lo-1 .. x_lo+w)."""
+
+    def __init__(self, spec: LatticeSpec, w: int | None = None, x_lo: int = 1, device: int = 0):
+        lib = _lib.load()
+        if lib.psg_device_count() <= 0:
+            raise DeviceError("no CUDA device visible: the hot path has no CPU fallback")
+        self.spec = spec
+        self.n = spec.N
+        self.w = spec.N if w is None else int(w)
+        self.x_lo = int(x_lo)
+        self.device = device
+        h = ctypes.c_void_p()
+        check(lib.psg_create(device, self.n, self.w, self.x_lo, spec.a, spec.m, spec.dtau,
+                             ctypes.byref(h)))
+        self._h = h
+        self._lib = lib
+        pitch, stride, planes = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        lib.psg_geometry(h, ctypes.byref(pitch), ctypes.byref(stride), ctypes.byref(planes))
+        self.pitch, self.plane_stride, self.planes = pitch.value, stride.value, planes.value
+        self._v_owner = None
+
+    # ------------------------------------------------------------ lifetime
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.psg_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def stream(self) -> int:
+        return int(self._lib.psg_stream(self._h) or 0)
+
+    def sync(self):
+        check(self._lib.psg_sync(self._h))
+
+    def launches(self) -> int:
+        return int(self._lib.psg_launch_count(self._h))
+
+    def tune(self, blocks_per_sm: int = 0, zchunk: int = 0):
+        check(self._lib.psg_tune(self._h, blocks_per_sm, zchunk))
+
+    # ------------------------------------------------------------ data
+    @property
+    def ext(self) -> int:
+        return self.n + 2
+
+    def _planes_arg(self, arr: np.ndarray) -> np.ndarray:
+        arr = np.ascontiguousarray(arr, dtype=np.float64)
+        if arr.ndim != 3 or arr.shape[1:] != (self.ext, self.ext):
+            raise ConfigError(f"expected (planes, {self.ext}, {self.ext}) float64, got {arr.shape}")
+        return arr
+
+    def set_field(self, planes: np.ndarray, first: int = 0):
+        """Upload dense padded planes into local planes first.. of both buffers."""
+        planes = self._planes_arg(planes)
+        check(self._lib.psg_set_field(self._h, dptr(planes), first, planes.shape[0]))
+
+    def get_field(self, first: int = 0, count: int | None = None) -> np.ndarray:
+        """Download local planes (materialised state)."""
+        count = self.planes - first if count is None else count
+        out = np.empty((count, self.ext, self.ext))
+        check(self._lib.psg_get_field(self._h, dptr(out), first, count))
+        return out
+
+    def set_potential(self, planes: np.ndarray, first: int = 0, owner=None):
+        planes = self._planes_arg(planes)
+        bad = np.zeros(3, dtype=np.int64)
+        rc = self._lib.psg_set_potential(self._h, dptr(planes), first, planes.shape[0], lptr(bad))
+        if rc == 5:
+            i, j, k = (int(x) for x in bad)
+            raise SingularCoefficientError(
+                f"1 + (dtau/2) V = 0 at site ({i},{j},{k}); the potential must be regulated")
+        check(rc)
+        self._v_owner = owner
+
+    def set_coefficients(self, a_planes: np.ndarray, c_planes: np.ndarray, first: int = 0):
+        a_planes = self._planes_arg(a_planes)
+        c_planes = self._planes_arg(c_planes)
+        check(self._lib.psg_set_coefficients(self._h, dptr(a_planes), dptr(c_planes), first,
+                                             a_planes.shape[0]))
+
+    def load_grid(self, grid):
+        """Upload V of a host PotentialGrid (whole lattice or this slab's part)."""
+        if self._v_owner is grid:
+            return
+        lo = self.x_lo - 1
+        self.set_potential(grid.v[lo:lo + self.planes], 0, owner=grid)
+
+    # ------------------------------------------------------------ compute
+    def sweep(self, z_lo: int = 1, z_hi: int | None = None, flags: int = F_WRITE):
+        z_hi = self.w if z_hi is None else z_hi
+        check(self._lib.psg_sweep(self._h, z_lo, z_hi, flags))
+
+    def swap(self, renorm: bool = False):
+        check(self._lib.psg_swap(self._h, 1 if renorm else 0))
+
+    def reduce(self, z_lo: int = 1, z_hi: int | None = None, flags: int = F_NORM,
+               combine: bool = True):
+        z_hi = self.w if z_hi is None else z_hi
+        check(self._lib.psg_reduce(self._h, z_lo, z_hi, flags, 1 if combine else 0))
+
+    def combine(self, flags: int):
+        check(self._lib.psg_combine(self._h, flags))
+
+    def measure(self, z_lo: int = 1, z_hi: int | None = None):
+        z_hi = self.w if z_hi is None else z_hi
+        check(self._lib.psg_measure(self._h, z_lo, z_hi))
+
+    def dot(self, other: "Slab", z_lo: int = 1, z_hi: int | None = None):
+        z_hi = self.w if z_hi is None else z_hi
+        check(self._lib.psg_dot(self._h, other._h, z_lo, z_hi))
+
+    def read_sums(self):
+        """(plane_sums[4][N], scalars[16]) after a reduce/combine."""
+        ps = np.empty((4, self.n))
+        sc = np.empty(NSCAL)
+        check(self._lib.psg_read_sums(self._h, dptr(ps), dptr(sc)))
+        return ps, sc
+
+    def plane_sums_ptr(self) -> int:
+        return int(self._lib.psg_plane_sums_ptr(self._h))
+
+    def plane_ptr(self, plane: int, which: int = 0) -> int:
+        return int(self._lib.psg_plane_ptr(self._h, which, plane))
+
+    def materialize(self):
+        check(self._lib.psg_materialize(self._h))
+
+    def scale(self, factor: float):
+        check(self._lib.psg_scale(self._h, float(factor)))
+
+    def impose(self, axis: int, sign: int, mode: int = 0):
+        check(self._lib.psg_impose(self._h, axis, sign, mode))
+
+    def resample_from(self, coarse: "Slab", i0: np.ndarray, frac: np.ndarray):
+        i0 = np.ascontiguousarray(i0, dtype=np.int64)
+        frac = np.ascontiguousarray(frac, dtype=np.float64)
+        check(self._lib.psg_resample(coarse._h, self._h, lptr(i0), dptr(frac)))
+
+    def run(self, steps: int, measure_every: int = 0, norm_every: int = 1,
+            reimpose_every: int = 0, impose_axis: int = 0, impose_sign: int = -1,
+            step_offset: int = 0, max_checks: int | None = None):
+        """Fused fixed-step driver (psg_run); returns (steps, plane sums [c,3,N], status)."""
+        p = RunParams(steps, measure_every, norm_every, reimpose_every, impose_axis, impose_sign,
+                      step_offset)
+        if max_checks is None:
+            max_checks = steps // measure_every + 1 if measure_every > 0 else 0
+        rec = 3 * self.n + 2
+        hist = np.zeros((max(max_checks, 1), rec))
+        nc = ctypes.c_int64()
+        check(self._lib.psg_run(self._h, ctypes.byref(p), dptr(hist), max_checks, ctypes.byref(nc)))
+        hist = hist[:nc.value]
+        return (hist[:, 0].astype(np.int64), hist[:, 2:].reshape(-1, 3, self.n),
+                hist[:, 1].astype(np.int64))

@@ -1,0 +1,108 @@
+"""GPU parity of the core kernels against the CPU oracle (bitwise where the
+reference's arithmetic is elementwise, tolerance-stated where it reduces)."""
+
+import math
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_0904_0939_b200.device import F_MEASURE, F_NORM, F_WRITE, Slab
+from paper_0904_0939_b200.lattice import LatticeSpec
+
+pytestmark = pytest.mark.gpu
+
+
+def _case(n, seed, a=0.7, m=1.3, dtau=0.05, vlo=-2.0, vhi=2.0, pad=0.0):
+    rng = np.random.default_rng(seed)
+    spec = LatticeSpec(N=n, a=a, m=m, dtau=dtau)
+    ext = n + 2
+    v = np.zeros((ext,) * 3)
+    v[1:-1, 1:-1, 1:-1] = rng.uniform(vlo, vhi, (n, n, n))
+    psi = rng.standard_normal((ext,) * 3)
+    if pad == 0.0:
+        psi[0] = psi[-1] = 0.0
+        psi[:, 0] = psi[:, -1] = 0.0
+        psi[:, :, 0] = psi[:, :, -1] = 0.0
+    return spec, psi, v
+
+
+@pytest.mark.parametrize("n", [4, 5, 9, 16, 63, 64, 65, 130])
+def test_sweep_bitwise(gpu_lib, n):
+    spec, psi, v = _case(n, 100 + n, pad=1.0)
+    want = psi.copy()
+    O.stencil_update_v(psi, v, spec.dtau, spec.m, spec.a, want, 1, n)
+    with Slab(spec) as s:
+        s.set_field(psi)
+        s.set_potential(v)
+        s.sweep(1, n, F_WRITE)
+        s.swap()
+        got = s.get_field()
+    assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("n", [8, 33, 128])
+def test_fused_norm_and_measure(gpu_lib, n):
+    spec, psi, v = _case(n, 7 + n)
+    out = psi.copy()
+    O.stencil_update_v(psi, v, spec.dtau, spec.m, spec.a, out, 1, n)
+    kin = 1.0 / (2.0 * spec.m * spec.a * spec.a)
+    num, den = O.energy_plane_sums(psi, v, kin, 1, n)
+    r2, _ = O.radius2_plane_sums(psi, 1, spec.center, spec.a, 1, n)
+    nrm = O.norm_plane_sums(out, 1, n)
+    with Slab(spec) as s:
+        s.set_field(psi)
+        s.set_potential(v)
+        s.sweep(1, n, F_WRITE | F_NORM | F_MEASURE)
+        s.reduce(1, n, F_NORM | F_MEASURE, combine=True)
+        ps, sc = s.read_sums()
+    # plane sums: same terms, different (tree) association -> 1e-13 relative
+    np.testing.assert_allclose(ps[0], num, rtol=1e-12, atol=1e-13 * np.abs(num).max())
+    np.testing.assert_allclose(ps[1], den, rtol=1e-13)
+    np.testing.assert_allclose(ps[2], r2, rtol=1e-13)
+    np.testing.assert_allclose(ps[3], nrm, rtol=1e-13)
+    # device pairwise combine == np.sum of the same vector, bitwise
+    for q in range(4):
+        assert sc[q] == float(np.sum(ps[q]))
+    e_ref = O.np_sum(num) / O.np_sum(den)
+    assert abs(sc[4] - e_ref) <= 1e-10 * abs(e_ref)
+    n2 = float(np.sum(ps[3])) * spec.a ** 3
+    assert sc[8] == 1.0 / math.sqrt(n2)
+
+
+def test_pairwise_device_matches_numpy(gpu_lib):
+    import ctypes
+    rng = np.random.default_rng(3)
+    for n in list(range(1, 40)) + [127, 128, 129, 255, 256, 257, 511, 512, 1000, 2048, 4099]:
+        a = rng.standard_normal(n) * np.exp(rng.uniform(-10, 10, n))
+        out = ctypes.c_double()
+        assert gpu_lib.psg_pairwise_sum_device(a.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                               n, ctypes.byref(out)) == 0
+        assert out.value == float(np.sum(a)), n
+
+
+@pytest.mark.parametrize("n,steps,check", [(16, 300, 50), (40, 400, 100)])
+def test_fixed_run_matches_oracle(gpu_lib, n, steps, check):
+    spec = LatticeSpec(N=n, a=0.3, m=1.0, dtau=0.3 * 0.3 / 4.0)
+    rng = np.random.default_rng(n)
+    ext = n + 2
+    psi0 = np.zeros((ext,) * 3)
+    psi0[1:-1, 1:-1, 1:-1] = rng.uniform(-0.5, 0.5, (n, n, n))
+    off = (np.arange(1, n + 1) - spec.center) * spec.a
+    r = np.sqrt((off[:, None, None] ** 2 + off[None, :, None] ** 2) + off[None, None, :] ** 2)
+    v = np.zeros((ext,) * 3)
+    v[1:-1, 1:-1, 1:-1] = 0.5 * r * r
+    want, checks = O.evolve_fixed(psi0, v, n, spec.a, spec.m, spec.dtau, steps, check)
+    with Slab(spec) as s:
+        s.set_field(psi0)
+        s.set_potential(v)
+        idx, sums, status = s.run(steps, measure_every=check, norm_every=1)
+        got = s.get_field()
+    assert np.abs(got - want).max() <= 1e-12 * np.abs(want).max()
+    assert list(idx) == [c[0] for c in checks]
+    assert not status.any()
+    for (st, e, n2, rr, num, den, r2), sm in zip(checks, sums):
+        e_gpu = float(np.sum(sm[0])) / float(np.sum(sm[1]))
+        assert abs(e_gpu - e) <= 1e-10 * abs(e)
+        rr_gpu = math.sqrt(float(np.sum(sm[2])) / float(np.sum(sm[1])))
+        assert abs(rr_gpu - rr) <= 1e-10 * abs(rr)
