@@ -82,6 +82,12 @@ int64_t psg_row_pitch(int64_t n);
  * combine must happen without a host round trip.  out[0] = sum(a[0..n)). */
 int psg_pairwise_sum_device(const double* host_a, int64_t n, double* out);
 
+/* Self-test of the sweep's shared-reciprocal coefficient division: compares
+ * A = (1-hv)/(1+hv) and B = 1/(1+hv) against IEEE division for `count`
+ * pseudo-random hv in [lo, hi); *mismatches = number of differing sites. */
+int psg_selftest_division(int64_t count, uint64_t seed, double lo, double hi,
+                          uint64_t* mismatches);
+
 /* ------------------------------------------------------------------ */
 /* 1. operator layer: kernels.py entry points on host arrays             */
 /* ------------------------------------------------------------------ */
@@ -187,13 +193,17 @@ int psg_reduce(psg_slab* s, int64_t z_lo, int64_t z_hi, unsigned flags, int comb
  * the zero-padded vectors across slabs). */
 double* psg_plane_sums_ptr(psg_slab* s);
 
+/* Zero the plane-sum vectors (before a slab's reduce + all-reduce). */
+int psg_zero_sums(psg_slab* s);
+
 /* Combine only (after an external all-reduce of the plane sums). */
 int psg_combine(psg_slab* s, unsigned flags);
 
 /* Copy the plane sums [4][n] and the scalars to the host:
  * scal[0..3] = totals (num, den, r2, norm), scal[4] = E, scal[5] = norm2
  * (den*a^3), scal[6] = r_rms, scal[7] = n2 (norm*a^3), scal[8] = next
- * factor 1/sqrt(n2), scal[9] = status (0 ok, 3 zero norm, 4 non-finite). */
+ * factor 1/sqrt(n2), scal[9] = status (0 ok, 3 zero norm, 4 non-finite),
+ * scal[12] = non-finite-output flag of the sweeps since psg_set_field. */
 int psg_read_sums(psg_slab* s, double* plane_sums, double* scal);
 
 /* Observables of the current state without updating it (energy_plane_sums +
@@ -204,14 +214,37 @@ int psg_measure(psg_slab* s, int64_t z_lo, int64_t z_hi);
  * state (dot_plane_sums, kernels.py:103-112), into PSG_Q_NUM. */
 int psg_dot(psg_slab* s, psg_slab* other, int64_t z_lo, int64_t z_hi);
 
+/* Norm partials (sum psi^2 per tile, PSG_Q_NORM) of the current state
+ * (norm_plane_sums, kernels.py:40-49), for psg_reduce(PSG_F_NORM). */
+int psg_norm_partials(psg_slab* s, int64_t z_lo, int64_t z_hi);
+
+/* Read the current state through the factor of the last combine from now on
+ * (SweepBuffers.renormalize's psi *= 1/sqrt(n2), folded into the next read). */
+int psg_use_factor(psg_slab* s);
+
+/* Read the current state through an explicit factor (slab engine: the factor
+ * is combined from all slabs' plane sums). */
+int psg_set_factor(psg_slab* s, double factor);
+
+/* psi_s <- psi_s - c * psi_o (both materialised), states._project_inplace
+ * (states.py:92-99). */
+int psg_axpy(psg_slab* s, psg_slab* o, double c);
+
+/* Copy one local plane between slabs (same or peer device), ordered on the
+ * destination stream after the source stream's pending work: the halo
+ * exchange of the single-process slab engine (parallel.halo_step,
+ * parallel.py:179-217). which: 0 current buffer, 1 other. */
+int psg_copy_plane(psg_slab* dst, int dst_which, int64_t dst_plane, psg_slab* src, int src_which,
+                   int64_t src_plane);
+
 /* Apply the pending normalisation to the stored state (psi *= f). */
 int psg_materialize(psg_slab* s);
 
 /* Scale the stored state by an explicit factor (renormalize(), evolve.py:56-64). */
 int psg_scale(psg_slab* s, double factor);
 
-/* Reflection-parity imposition on a slab that holds the whole lattice
- * (w == n): mode 0 = copy (states.impose_inplace, states.py:70-82),
+/* Reflection-parity imposition (axis 0 needs the whole lattice on the slab,
+ * w == n; axes 1 and 2 act within every plane of any slab): mode 0 = copy (states.impose_inplace, states.py:70-82),
  * mode 1 = projector psi <- (psi + sign * R psi) * 0.5.  axis 0/1/2 is the
  * storage axis, sign = +1 / -1.  The pending scale is applied on the fly. */
 int psg_impose(psg_slab* s, int axis, int sign, int mode);
@@ -228,10 +261,12 @@ typedef struct psg_run_params {
   int64_t steps;          /* sweeps to run */
   int64_t measure_every;  /* observables on the state entering sweep s when (s-1) % m == 0, s>1; 0 = never */
   int64_t norm_every;     /* renormalise after sweep s when s % k == 0; 0 = never */
-  int64_t reimpose_every; /* impose after sweep s when s % r == 0; 0 = never */
-  int32_t impose_axis;    /* storage axis of the constraint */
-  int32_t impose_sign;    /* +1 / -1 */
-  int64_t step_offset;    /* index of the first sweep minus one (for resumed runs) */
+  int64_t reimpose_every; /* impose the constraints after sweep s when s % r == 0; 0 = never */
+  int64_t step_offset;    /* sweeps already done before this call (s counts from step_offset+1) */
+  int32_t n_impose;       /* number of parity constraints (0..3), applied in order */
+  int32_t impose_axis[3]; /* storage axis of each constraint */
+  int32_t impose_sign[3]; /* +1 symmetric / -1 antisymmetric */
+  int32_t reserved;
 } psg_run_params;
 
 /* Fused fixed-step driver: runs the evolve_to_convergence loop body
@@ -242,8 +277,9 @@ typedef struct psg_run_params {
 int psg_run(psg_slab* s, const psg_run_params* p, double* hist, int64_t max_checks,
             int64_t* n_checks);
 
-/* Kernel tuning knobs (0 = keep): blocks per SM for the sweep, z chunk. */
-int psg_tune(psg_slab* s, int blocks_per_sm, int zchunk);
+/* Kernel tuning knobs (0 = automatic): sweep blocks per SM, z-chunk length
+ * (planes per work item), pipeline depth (planes in flight per block: 4/6/8). */
+int psg_tune(psg_slab* s, int blocks_per_sm, int zchunk, int stages);
 
 /* Number of kernels this slab has launched so far. */
 int64_t psg_launch_count(psg_slab* s);

@@ -38,9 +38,11 @@ class RunParams(ctypes.Structure):
         ("measure_every", c_int64),
         ("norm_every", c_int64),
         ("reimpose_every", c_int64),
-        ("impose_axis", c_int32),
-        ("impose_sign", c_int32),
         ("step_offset", c_int64),
+        ("n_impose", c_int32),
+        ("impose_axis", c_int32 * 3),
+        ("impose_sign", c_int32 * 3),
+        ("reserved", c_int32),
     ]
 
 
@@ -51,6 +53,8 @@ SIGNATURES = {
     "psg_device_count": (c_int, []),
     "psg_row_pitch": (c_int64, [c_int64]),
     "psg_pairwise_sum_device": (c_int, [_dp, c_int64, _dp]),
+    "psg_selftest_division": (c_int, [c_int64, ctypes.c_uint64, c_double, c_double,
+                                      POINTER(ctypes.c_uint64)]),
     "psg_kernel_stencil_update": (c_int, [_dp, _dp, _dp, _dp, c_int64, c_int64, c_int64, c_int64]),
     "psg_kernel_stencil_update_v": (
         c_int, [_dp, _dp, c_double, c_double, c_double, _dp, c_int64, c_int64, c_int64, c_int64]),
@@ -84,7 +88,13 @@ SIGNATURES = {
     "psg_impose": (c_int, [c_void_p, c_int, c_int, c_int]),
     "psg_resample": (c_int, [c_void_p, c_void_p, _lp, _dp]),
     "psg_run": (c_int, [c_void_p, POINTER(RunParams), _dp, c_int64, _lp]),
-    "psg_tune": (c_int, [c_void_p, c_int, c_int]),
+    "psg_tune": (c_int, [c_void_p, c_int, c_int, c_int]),
+    "psg_norm_partials": (c_int, [c_void_p, c_int64, c_int64]),
+    "psg_use_factor": (c_int, [c_void_p]),
+    "psg_zero_sums": (c_int, [c_void_p]),
+    "psg_set_factor": (c_int, [c_void_p, c_double]),
+    "psg_axpy": (c_int, [c_void_p, c_void_p, c_double]),
+    "psg_copy_plane": (c_int, [c_void_p, c_int, c_int64, c_void_p, c_int, c_int64]),
     "psg_launch_count": (c_int64, [c_void_p]),
 }
 

@@ -20,6 +20,16 @@ from .lattice import LatticeSpec
 __all__ = ["Slab", "F_WRITE", "F_NORM", "F_MEASURE"]
 
 
+class _DeviceArray:
+    """__cuda_array_interface__ view of device memory owned by a slab, so
+    torch (NCCL collectives, P2P) can address it without a copy."""
+
+    def __init__(self, ptr: int, count: int):
+        self.__cuda_array_interface__ = {"shape": (count,), "typestr": "<f8",
+                                         "data": (ptr, False), "version": 3,
+                                         "strides": None, "stream": None}
+
+
 class Slab:
     """One GPU's slab of local planes 0..w+1 (global x_lo-1 .. x_lo+w)."""
 
@@ -74,8 +84,8 @@ class Slab:
     def launches(self) -> int:
         return int(self._lib.psg_launch_count(self._h))
 
-    def tune(self, blocks_per_sm: int = 0, zchunk: int = 0):
-        check(self._lib.psg_tune(self._h, blocks_per_sm, zchunk))
+    def tune(self, blocks_per_sm: int = 0, zchunk: int = 0, stages: int = 0):
+        check(self._lib.psg_tune(self._h, blocks_per_sm, zchunk, stages))
 
     # ------------------------------------------------------------ data
     @property
@@ -161,6 +171,56 @@ class Slab:
     def plane_ptr(self, plane: int, which: int = 0) -> int:
         return int(self._lib.psg_plane_ptr(self._h, which, plane))
 
+    def zero_sums(self):
+        check(self._lib.psg_zero_sums(self._h))
+
+    # ---- torch views (NCCL plumbing) -----------------------------------------
+    def torch_device(self):
+        import torch
+
+        return torch.device("cuda", self.device)
+
+    def plane_tensor(self, plane: int, which: int = 0):
+        """torch view of local plane `plane` of the current (0) / other (1) buffer."""
+        import torch
+
+        ptr = self.plane_ptr(plane, which)
+        if not ptr:
+            raise ConfigError(f"plane {plane} outside the slab")
+        return torch.as_tensor(_DeviceArray(ptr, self.plane_stride), device=self.torch_device())
+
+    def sums_tensor(self):
+        """torch view of the [4][N] plane-sum vectors."""
+        import torch
+
+        return torch.as_tensor(_DeviceArray(self.plane_sums_ptr(), 4 * self.n),
+                               device=self.torch_device())
+
+    def stream_ctx(self):
+        """Make the slab's stream torch's current stream (NCCL ops order on it)."""
+        import torch
+
+        return torch.cuda.stream(torch.cuda.ExternalStream(self.stream, device=self.torch_device()))
+
+    def norm_partials(self, z_lo: int = 1, z_hi: int | None = None):
+        z_hi = self.w if z_hi is None else z_hi
+        check(self._lib.psg_norm_partials(self._h, z_lo, z_hi))
+
+    def use_factor(self):
+        check(self._lib.psg_use_factor(self._h))
+
+    def set_factor(self, factor: float):
+        check(self._lib.psg_set_factor(self._h, float(factor)))
+
+    def axpy(self, other: "Slab", c: float):
+        """psi <- psi - c * other.psi (states._project_inplace, states.py:92-99)."""
+        check(self._lib.psg_axpy(self._h, other._h, float(c)))
+
+    def copy_plane_from(self, dst_plane: int, src: "Slab", src_plane: int, dst_which: int = 0,
+                        src_which: int = 0):
+        check(self._lib.psg_copy_plane(self._h, dst_which, dst_plane, src._h, src_which,
+                                       src_plane))
+
     def materialize(self):
         check(self._lib.psg_materialize(self._h))
 
@@ -176,11 +236,20 @@ class Slab:
         check(self._lib.psg_resample(coarse._h, self._h, lptr(i0), dptr(frac)))
 
     def run(self, steps: int, measure_every: int = 0, norm_every: int = 1,
-            reimpose_every: int = 0, impose_axis: int = 0, impose_sign: int = -1,
-            step_offset: int = 0, max_checks: int | None = None):
-        """Fused fixed-step driver (psg_run); returns (steps, plane sums [c,3,N], status)."""
-        p = RunParams(steps, measure_every, norm_every, reimpose_every, impose_axis, impose_sign,
-                      step_offset)
+            reimpose_every: int = 0, constraints=(), step_offset: int = 0,
+            max_checks: int | None = None):
+        """Fused fixed-step driver (psg_run).
+
+        constraints: sequence of (storage axis, sign) applied in order every
+        reimpose_every sweeps.  Returns (state indices, plane sums [c, 3, N]
+        as num|den|r2, per-check status)."""
+        constraints = list(constraints)
+        if len(constraints) > 3:
+            raise ConfigError("at most 3 parity constraints")
+        axes = (ctypes.c_int32 * 3)(*([c[0] for c in constraints] + [0] * (3 - len(constraints))))
+        signs = (ctypes.c_int32 * 3)(*([int(c[1]) for c in constraints] + [1] * (3 - len(constraints))))
+        p = RunParams(steps, measure_every, norm_every, reimpose_every, step_offset,
+                      len(constraints), axes, signs, 0)
         if max_checks is None:
             max_checks = steps // measure_every + 1 if measure_every > 0 else 0
         rec = 3 * self.n + 2
@@ -190,3 +259,7 @@ class Slab:
         hist = hist[:nc.value]
         return (hist[:, 0].astype(np.int64), hist[:, 2:].reshape(-1, 3, self.n),
                 hist[:, 1].astype(np.int64))
+
+    def status(self) -> int:
+        """Sticky device status: 0 ok, 3 zero norm, 4 non-finite (read_sums scal[9])."""
+        return int(self.read_sums()[1][9])

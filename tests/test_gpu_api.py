@@ -1,0 +1,485 @@
+"""The psibox-compatible API on the GPU: the reference's own test strategy
+(pkg/tests/test_evolve.py, test_observables.py, test_states.py) ported onto
+paper_0904_0939_b200, plus parity against fixtures generated from the
+reference (tests/golden/) and the slab engine's bitwise M-invariance."""
+
+import math
+import os
+
+import numpy as np
+import pytest
+
+import dense
+from paper_0904_0939_b200 import (LatticeSpec, SymmetryConstraint, allocate, binding_energy,
+                                  check_stability, coulomb, energy, evolve_fixed,
+                                  evolve_parallel, evolve_to_convergence, fill_random_gaussian,
+                                  harmonic, impose, impose_inplace, kernels, norm2, overlap,
+                                  project, project_out, renormalize, resample, rms_radius, step,
+                                  symmetry_excited_run, workloads)
+from paper_0904_0939_b200.errors import (ConfigError, DegenerateSnapshotError, DivergenceError,
+                                         ExtractionError, ZeroNormError)
+from paper_0904_0939_b200.evolve import SweepBuffers
+from paper_0904_0939_b200.lattice import Field3D
+from paper_0904_0939_b200.potential import custom
+from paper_0904_0939_b200.states import extract_excited
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def gold(name):
+    return np.load(os.path.join(GOLD, name + ".npz"))
+
+
+def free_box(n, a=1.0, dtau=None):
+    spec = LatticeSpec(N=n, a=a, m=1.0, dtau=dtau if dtau else a * a / 4.0)
+    return spec, custom(spec, np.zeros((n, n, n)))
+
+
+def box_spec(n, a=1.0):
+    return LatticeSpec(N=n, a=a, m=1.0, dtau=a * a / 4.0)
+
+
+# ---------------------------------------------------------------- step (test_evolve.py)
+class TestStep:
+    def test_zero_field(self, gpu_lib):
+        spec, grid = free_box(5)
+        assert not step(allocate(spec), grid).values.any()
+
+    def test_single_site_hand_values(self, gpu_lib):
+        spec, grid = free_box(5, a=1.0, dtau=0.1)
+        f = allocate(spec)
+        f.values[3, 3, 3] = 1.0
+        out = step(f, grid)
+        assert out.values[3, 3, 3] == pytest.approx(0.7, abs=1e-15)
+        for s in ((4, 3, 3), (2, 3, 3), (3, 4, 3), (3, 2, 3), (3, 3, 4), (3, 3, 2)):
+            assert out.values[s] == pytest.approx(0.05, abs=1e-16)
+        assert (out.interior != 0).sum() == 7
+
+    def test_matches_dense_update_operator(self, gpu_lib):
+        rng = np.random.default_rng(31)
+        n = 4
+        spec = LatticeSpec(N=n, a=0.7, m=1.3, dtau=0.05)
+        v = rng.uniform(-2.0, 2.0, size=(n, n, n))
+        grid = custom(spec, v)
+        f = dense.to_field(spec, rng.standard_normal(n ** 3))
+        got = dense.to_vec(step(f, grid))
+        want = dense.update_operator(spec, v) @ dense.to_vec(f)
+        np.testing.assert_allclose(got, want, rtol=1e-15, atol=1e-15 * np.abs(want).max())
+
+    def test_linearity(self, gpu_lib):
+        rng = np.random.default_rng(5)
+        spec, _ = free_box(6, a=0.5)
+        grid = custom(spec, rng.uniform(-1.0, 1.0, size=(6, 6, 6)))
+        f1 = dense.to_field(spec, rng.standard_normal(216))
+        f2 = dense.to_field(spec, rng.standard_normal(216))
+        combo = dense.to_field(spec, 1.7 * dense.to_vec(f1) - 0.4 * dense.to_vec(f2))
+        lhs = dense.to_vec(step(combo, grid))
+        rhs = 1.7 * dense.to_vec(step(f1, grid)) - 0.4 * dense.to_vec(step(f2, grid))
+        np.testing.assert_allclose(lhs, rhs, rtol=1e-13, atol=1e-15)
+
+    def test_padding_carried_over(self, gpu_lib):
+        spec, grid = free_box(4)
+        f = fill_random_gaussian(allocate(spec), 1)
+        f.values[0, :, :] = 3.5
+        out = step(f, grid)
+        assert (out.values[0, :, :] == 3.5).all()
+
+    def test_nonfinite_raises(self, gpu_lib):
+        spec, grid = free_box(4)
+        f = allocate(spec)
+        f.interior[0, 0, 0] = np.inf
+        with pytest.raises(DivergenceError):
+            step(f, grid)
+
+
+class TestRenormalize:
+    def test_sets_unit_norm(self, gpu_lib):
+        spec, _ = free_box(6, a=0.5)
+        out, _ = renormalize(fill_random_gaussian(allocate(spec), 9))
+        assert norm2(out) == pytest.approx(1.0, abs=1e-13)
+
+    def test_idempotent_on_normalized(self, gpu_lib):
+        spec, _ = free_box(6, a=0.5)
+        f, _ = renormalize(fill_random_gaussian(allocate(spec), 9))
+        again, nrm = renormalize(f)
+        assert nrm == pytest.approx(1.0, abs=1e-13)
+        np.testing.assert_allclose(again.values, f.values, rtol=1e-15, atol=0)
+
+    def test_homogeneity(self, gpu_lib):
+        spec, _ = free_box(6, a=0.5)
+        f = fill_random_gaussian(allocate(spec), 9)
+        base, n1 = renormalize(f)
+        scaled = f.copy()
+        scaled.values *= 7.0
+        out, n7 = renormalize(scaled)
+        assert n7 == pytest.approx(7.0 * n1, rel=1e-13)
+        np.testing.assert_allclose(out.values, base.values, rtol=1e-14, atol=0)
+
+    def test_zero_field_rejected(self, gpu_lib):
+        spec, _ = free_box(4)
+        with pytest.raises(ZeroNormError):
+            renormalize(allocate(spec))
+
+
+class TestConvergence:
+    def test_free_box_matches_dense_ground_state(self, gpu_lib):
+        spec, grid = free_box(8, a=1.0)
+        vals, _ = dense.lowest(dense.hamiltonian(spec, np.zeros((8, 8, 8))), 1)
+        st = evolve_to_convergence(fill_random_gaussian(allocate(spec), 3), grid, tol=1e-9,
+                                   check_freq=50, max_steps=20000)
+        assert st.converged
+        assert st.energy == pytest.approx(vals[0], abs=1e-6)
+
+    def test_energy_monotone_after_transient(self, gpu_lib):
+        n = 16
+        spec = LatticeSpec(N=n, a=0.4, m=1.0, dtau=0.4 * 0.4 / 4)
+        off = (np.arange(1, n + 1) - spec.center) * spec.a
+        r2 = off[:, None, None] ** 2 + off[None, :, None] ** 2 + off[None, None, :] ** 2
+        grid = custom(spec, 0.5 * r2, unbounded=True)
+        st = evolve_to_convergence(fill_random_gaussian(allocate(spec), 17), grid, tol=1e-8,
+                                   check_freq=20, max_steps=20000)
+        e = [c.energy for c in st.checks]
+        start = next(i for i in range(1, len(e)) if abs(e[i] - e[i - 1]) < 1e-3 * abs(e[i]))
+        for prev, cur in zip(e[start:], e[start + 1:]):
+            assert cur <= prev + 1e-10
+
+    def test_eigenvector_is_fixed_point(self, gpu_lib):
+        spec, grid = free_box(6, a=1.0, dtau=0.2)
+        vals, vecs = dense.lowest(dense.hamiltonian(spec, np.zeros((6, 6, 6))), 4)
+        for idx in (0, 3):
+            f = dense.to_field(spec, vecs[:, idx])
+            assert abs(energy(step(f, grid), grid) - energy(f, grid)) < 1e-12
+
+    def test_max_steps_returns_unconverged(self, gpu_lib):
+        spec, grid = free_box(6, a=1.0)
+        st = evolve_to_convergence(fill_random_gaussian(allocate(spec), 1), grid, tol=1e-14,
+                                   check_freq=10, max_steps=40)
+        assert not st.converged and st.step_count == 40
+
+    def test_zero_start_rejected(self, gpu_lib):
+        spec, grid = free_box(6, a=1.0)
+        with pytest.raises(ZeroNormError):
+            evolve_to_convergence(allocate(spec), grid, check_freq=10, max_steps=50)
+
+    def test_unstable_step_diverges_within_500(self, gpu_lib):
+        spec = LatticeSpec(N=12, a=1.0, m=1.0, dtau=1.05 / 3.0)
+        grid = custom(spec, np.zeros((12, 12, 12)))
+        assert not check_stability(spec).ok
+        with pytest.raises(DivergenceError):
+            evolve_to_convergence(fill_random_gaussian(allocate(spec), 4), grid, tol=1e-6,
+                                  check_freq=100, max_steps=500)
+
+    def test_prenorm_growth_when_unstable(self, gpu_lib):
+        spec = LatticeSpec(N=12, a=1.0, m=1.0, dtau=1.05 / 3.0)
+        grid = custom(spec, np.zeros((12, 12, 12)))
+        work = SweepBuffers(fill_random_gaussian(allocate(spec), 4).values)
+        norms = []
+        for _ in range(500):
+            work.sweep(grid, 12)
+            norms.append(work.renormalize(spec))
+        tail = norms[-50:]
+        assert all(b > a for a, b in zip(tail, tail[1:]))
+        assert tail[-1] > 1.0
+        work.close()
+
+    def test_stable_step_converges(self, gpu_lib):
+        spec = LatticeSpec(N=12, a=1.0, m=1.0, dtau=0.25)
+        grid = custom(spec, np.zeros((12, 12, 12)))
+        st = evolve_to_convergence(fill_random_gaussian(allocate(spec), 4), grid, tol=1e-7,
+                                   check_freq=100, max_steps=20000)
+        assert st.converged
+
+    def test_snapshot_schedule_and_cap(self, gpu_lib):
+        spec, grid = free_box(6, a=1.0)
+        st = evolve_to_convergence(fill_random_gaussian(allocate(spec), 2), grid, tol=1e-14,
+                                   check_freq=10, snap_freq=25, max_steps=200, max_snapshots=5)
+        taus = [t for t, _ in st.snapshots]
+        assert taus == pytest.approx([25 * spec.dtau * k for k in range(1, 6)])
+
+    def test_tau_tracks_step_count(self, gpu_lib):
+        spec, grid = free_box(6, a=1.0)
+        st = evolve_to_convergence(fill_random_gaussian(allocate(spec), 2), grid, tol=1e-14,
+                                   check_freq=10, max_steps=30)
+        assert st.tau == pytest.approx(st.step_count * spec.dtau)
+
+
+# ---------------------------------------------------------------- observables
+class TestObservables:
+    def test_single_site_energy(self, gpu_lib):
+        spec = box_spec(5)
+        v = np.zeros((5, 5, 5))
+        v[2, 2, 2] = 1.7
+        f = allocate(spec)
+        f.values[3, 3, 3] = 1.0
+        assert energy(f, custom(spec, v)) == pytest.approx(4.7, rel=1e-14)
+
+    def test_dense_eigenvectors(self, gpu_lib):
+        rng = np.random.default_rng(12)
+        spec = box_spec(6, a=0.8)
+        v = rng.uniform(-1.5, 1.5, size=(6, 6, 6))
+        grid = custom(spec, v)
+        vals, vecs = dense.lowest(dense.hamiltonian(spec, v), 3)
+        for i in range(3):
+            assert energy(dense.to_field(spec, vecs[:, i]), grid) == pytest.approx(vals[i], abs=1e-12)
+
+    def test_scale_invariance(self, gpu_lib):
+        rng = np.random.default_rng(3)
+        spec = box_spec(6, a=0.5)
+        grid = custom(spec, rng.uniform(-1, 1, size=(6, 6, 6)))
+        f = dense.to_field(spec, rng.standard_normal(216))
+        e = energy(f, grid)
+        for c in (-1.0, 3.0, 1e-8):
+            fc = dense.to_field(spec, c * dense.to_vec(f))
+            assert energy(fc, grid) == pytest.approx(e, rel=1e-12)
+            assert rms_radius(fc) == pytest.approx(rms_radius(f), rel=1e-12)
+
+    def test_rayleigh_bound(self, gpu_lib):
+        rng = np.random.default_rng(44)
+        for n, a in ((4, 1.0), (6, 0.7)):
+            spec = box_spec(n, a)
+            v = rng.uniform(-2, 2, size=(n, n, n))
+            lam = dense.lowest(dense.hamiltonian(spec, v), 1)[0][0]
+            for _ in range(3):
+                f = dense.to_field(spec, rng.standard_normal(n ** 3))
+                assert energy(f, custom(spec, v)) >= lam - 1e-12
+
+    def test_binding(self, gpu_lib):
+        spec = LatticeSpec(N=8, a=0.5, m=1.0, dtau=0.05)
+        g = coulomb(spec)
+        f = fill_random_gaussian(allocate(spec), 6)
+        assert binding_energy(f, g) == pytest.approx(energy(f, g) - 1.0 / spec.a, rel=1e-12)
+        assert binding_energy(f, harmonic(spec)) is None
+
+    def test_norm_and_rms(self, gpu_lib):
+        assert norm2(allocate(box_spec(4))) == 0.0
+        f = allocate(box_spec(5, a=1.0))
+        f.values[2, 3, 4] = 2.0
+        assert norm2(f) == 4.0
+        spec = box_spec(6, a=0.5)
+        f = allocate(spec)
+        f.values[2, 3, 5] = 1.3
+        c = spec.center
+        r0 = np.sqrt((2 - c) ** 2 + (3 - c) ** 2 + (5 - c) ** 2) * spec.a
+        assert rms_radius(f) == pytest.approx(r0, rel=1e-14)
+        with pytest.raises(ZeroNormError):
+            rms_radius(allocate(box_spec(4)))
+        with pytest.raises(ZeroNormError):
+            energy(allocate(box_spec(4)), custom(box_spec(4), np.zeros((4, 4, 4))))
+
+    def test_box_ground_state_rms(self, gpu_lib):
+        n = 16
+        spec = box_spec(n, a=0.5)
+        hop = 1.0 / (2.0 * spec.a * spec.a)
+        h1 = np.diag(np.full(n, 2.0 * hop)) - hop * (np.eye(n, k=1) + np.eye(n, k=-1))
+        g = np.linalg.eigh(h1)[1][:, 0]
+        vec = np.einsum("i,j,k->ijk", g, g, g).reshape(-1)
+        assert rms_radius(dense.to_field(spec, vec)) == pytest.approx(dense.rms_loop(spec, vec),
+                                                                       rel=1e-10)
+
+
+# ---------------------------------------------------------------- states
+class TestStates:
+    def test_z_column_copy_semantics(self, gpu_lib):
+        f = allocate(box_spec(4))
+        f.values[2, 3, 1:5] = [1.5, -2.0, 0.25, 4.0]
+        out = impose(f, SymmetryConstraint("z", "antisymmetric"))
+        np.testing.assert_array_equal(out.values[2, 3, 1:5], [1.5, -2.0, 2.0, -1.5])
+
+    def test_impose_matches_reference_bitwise(self, gpu_lib):
+        g = gold("states")
+        for n in (6, 7):
+            spec = box_spec(n)
+            for axis in "xyz":
+                for parity in ("symmetric", "antisymmetric"):
+                    c = SymmetryConstraint(axis, parity)
+                    out = impose(Field3D(spec, g[f"n{n}_in"].copy()), c)
+                    assert np.array_equal(out.values, g[f"n{n}_{axis}_{parity}"])
+                    again = g[f"n{n}_in"].copy()
+                    impose_inplace(again, n, c)
+                    assert np.array_equal(again, out.values)
+
+    def test_projector_is_odd_and_idempotent(self, gpu_lib):
+        spec = box_spec(8)
+        f = fill_random_gaussian(allocate(spec), 5)
+        c = SymmetryConstraint("x", "antisymmetric")
+        p1 = project(f, c)
+        assert np.array_equal(p1.values, -p1.values[::-1, :, :])
+        want = (f.values - f.values[::-1, :, :]) * 0.5
+        assert np.array_equal(p1.values, want)
+
+    def test_parity_preserved_without_reimposition(self, gpu_lib):
+        n = 8
+        spec = box_spec(n, a=0.6)
+        off = (np.arange(1, n + 1) - spec.center) * spec.a
+        r2 = off[:, None, None] ** 2 + off[None, :, None] ** 2 + off[None, None, :] ** 2
+        grid = custom(spec, 0.5 * r2)
+        init = fill_random_gaussian(allocate(spec), 21)
+        impose_inplace(init.values, n, SymmetryConstraint("z", "antisymmetric"))
+        st = evolve_to_convergence(init, grid, tol=1e-30, check_freq=1000, max_steps=100)
+        v = st.psi.values
+        assert np.abs(v[1:-1, 1:-1, 1:-1] + v[1:-1, 1:-1, -2:0:-1]).max() < 1e-12
+
+    def test_project_out(self, gpu_lib):
+        spec = box_spec(8, a=0.5)
+        b1, _ = renormalize(fill_random_gaussian(allocate(spec), 1))
+        b2, _ = renormalize(project_out(renormalize(fill_random_gaussian(allocate(spec), 2))[0], [b1]))
+        out = project_out(fill_random_gaussian(allocate(spec), 3), [b1, b2])
+        for b in (b1, b2):
+            assert abs(overlap(out, b)) < 1e-10 * math.sqrt(norm2(out))
+        with pytest.raises(DegenerateSnapshotError):
+            project_out(b1.copy(), [b1])
+        with pytest.raises(ConfigError):
+            project_out(fill_random_gaussian(allocate(spec), 2),
+                        [fill_random_gaussian(allocate(spec), 1)])
+
+    def test_first_excited_matches_dense(self, gpu_lib):
+        spec, grid = free_box(8, a=1.0)
+        st = evolve_to_convergence(fill_random_gaussian(allocate(spec), 3), grid, tol=1e-10,
+                                   check_freq=25, snap_freq=50, max_steps=30000,
+                                   max_snapshots=8)
+        assert st.converged
+        vals, _ = dense.lowest(dense.hamiltonian(spec, np.zeros((8, 8, 8))), 2)
+        (psi1, e1), = extract_excited(st, grid, 1, polish_steps=1500, check_freq=50)
+        assert e1 == pytest.approx(vals[1], abs=1e-5)
+        assert abs(overlap(psi1, st.psi)) < 1e-10
+        with pytest.raises(ExtractionError):
+            unconv = evolve_to_convergence(fill_random_gaussian(allocate(spec), 1), grid,
+                                           tol=1e-14, check_freq=10, snap_freq=10, max_steps=30)
+            extract_excited(unconv, grid, 1)
+
+    def test_antisymmetric_sector_matches_dense(self, gpu_lib):
+        spec, grid = free_box(8, a=1.0)
+        vals, _ = dense.lowest(dense.hamiltonian(spec, np.zeros((8, 8, 8))), 2)
+        psi1, e1, st = symmetry_excited_run(grid, [SymmetryConstraint("z", "antisymmetric")],
+                                            seed=8, tol=1e-10, check_freq=25, max_steps=30000)
+        assert e1 == pytest.approx(vals[1], abs=1e-5)
+        v = st.psi.values
+        assert np.abs(v[1:-1, 1:-1, 1:-1] + v[1:-1, 1:-1, -2:0:-1]).max() < 1e-12
+
+
+# ---------------------------------------------------------------- reference fixtures
+class TestGolden:
+    @pytest.mark.parametrize("n", [4, 5, 8, 13])
+    def test_kernels_api(self, gpu_lib, n):
+        g = gold("kernels")
+        psi, v = g[f"n{n}_psi"], g[f"n{n}_v"]
+        _, a, m, dtau = g[f"n{n}_spec"]
+        out = psi.copy()
+        kernels.stencil_update(psi, g[f"n{n}_coef_a"], g[f"n{n}_coef_c"], out, 1, n)
+        assert np.array_equal(out, g[f"n{n}_update"])
+        out2 = psi.copy()
+        kernels.stencil_update_v(psi, v, dtau, m, a, out2, 1, n)
+        assert np.array_equal(out2, g[f"n{n}_update"])
+        # plane sums: same terms, tree order on the device (1e-13 relative)
+        nrm = np.empty(n)
+        kernels.norm_plane_sums(psi, 1, n, nrm)
+        np.testing.assert_allclose(nrm, g[f"n{n}_norm"], rtol=1e-13)
+        num, den = np.empty(n), np.empty(n)
+        kernels.energy_plane_sums(psi, v, 1.0 / (2.0 * m * a * a), 1, n, num, den)
+        np.testing.assert_allclose(den, g[f"n{n}_den"], rtol=1e-13)
+        np.testing.assert_allclose(num, g[f"n{n}_num"], rtol=1e-12,
+                                   atol=1e-13 * np.abs(g[f"n{n}_num"]).max())
+        r2, _ = np.empty(n), np.empty(n)
+        kernels.radius2_plane_sums(psi, 1, 0.5 * (n + 1), a, 1, n, r2, np.empty(n))
+        np.testing.assert_allclose(r2, g[f"n{n}_r2"], rtol=1e-13)
+        sub = np.ascontiguousarray(psi[1:n + 1])
+        r2s, dens = np.empty(n - 3), np.empty(n - 3)
+        kernels.radius2_plane_sums(sub, 3, 0.5 * (n + 1), a, 1, n - 3, r2s, dens)
+        np.testing.assert_allclose(r2s, g[f"n{n}_r2_slab"], rtol=1e-13)
+        dot = np.empty(n)
+        kernels.dot_plane_sums(psi, g[f"n{n}_psi2"], 1, n, dot)
+        np.testing.assert_allclose(dot, g[f"n{n}_dot"], rtol=1e-12,
+                                   atol=1e-13 * np.abs(g[f"n{n}_dot"]).max())
+        spec = LatticeSpec(N=n, a=a, m=m, dtau=dtau)
+        f = Field3D(spec, psi)
+        assert energy(f, custom(spec, v[1:-1, 1:-1, 1:-1])) == pytest.approx(
+            g[f"n{n}_energy"][0], rel=1e-13)
+        assert norm2(f) == pytest.approx(g[f"n{n}_norm2"][0], rel=1e-14)
+        assert rms_radius(f) == pytest.approx(g[f"n{n}_rms"][0], rel=1e-14)
+
+    def test_resample(self, gpu_lib):
+        g = gold("resample")
+        cs = LatticeSpec(N=8, a=1.5, m=1.0, dtau=1.5 * 1.5 / 4)
+        for nf, af, key in ((16, 0.75, "fine16"), (12, 1.0, "fine12")):
+            fs = LatticeSpec(N=nf, a=af, m=1.0, dtau=af * af / 4)
+            out = resample(Field3D(cs, g["coarse"]), fs)
+            np.testing.assert_allclose(out.values, g[key], rtol=1e-14, atol=0)
+
+    def test_evolve_harmonic(self, gpu_lib):
+        g = gold("evolve")
+        spec = LatticeSpec(N=10, a=0.6, m=1.0, dtau=0.6 * 0.6 / 4)
+        st = evolve_to_convergence(Field3D(spec, g["h10_init"].copy()), harmonic(spec),
+                                   tol=1e-300, check_freq=50, max_steps=300, max_snapshots=0)
+        want = g["h10_psi"]
+        assert np.abs(st.psi.values - want).max() <= 1e-12 * np.abs(want).max()
+        for c, w in zip(st.checks, g["h10_checks"]):
+            assert c.step == w[0]
+            assert abs(c.energy - w[1]) <= 1e-10 * abs(w[1])
+            assert abs(c.r_rms - w[3]) <= 1e-10 * abs(w[3])
+
+    def test_evolve_antisym_reimpose(self, gpu_lib):
+        g = gold("evolve")
+        spec = LatticeSpec(N=10, a=0.8, m=1.0, dtau=0.8 * 0.8 / 4)
+        from paper_0904_0939_b200.potential import _radii
+
+        grid = custom(spec, -1.0 / np.maximum(_radii(spec), 0.5 * spec.a))
+        c = SymmetryConstraint("x", "antisymmetric")
+        st = evolve_to_convergence(Field3D(spec, g["a10_init"].copy()), grid, tol=1e-300,
+                                   check_freq=40, max_steps=240, constraints=[c],
+                                   max_snapshots=0, reimpose_freq=40)
+        want = g["a10_psi"]
+        assert np.abs(st.psi.values - want).max() <= 1e-12 * np.abs(want).max()
+        for rec, w in zip(st.checks, g["a10_checks"]):
+            assert abs(rec.energy - w[1]) <= 1e-10 * abs(w[1])
+
+    def test_config1_end_to_end(self, gpu_lib):
+        """BASELINE config 1 (64^3 harmonic, 2000 steps) against the reference run."""
+        g = gold("config1")
+        w = workloads.CONFIGS["C1"]
+        init = workloads.uniform_field(w.spec)
+        grid = workloads.make_grid(w)
+        for norm_every in (1, w.measure_every):
+            st = evolve_fixed(init, grid, w.steps, w.measure_every, norm_every=norm_every)
+            psi = st.psi.values
+            idx = g["sample_idx"]
+            got = psi[idx[:, 0], idx[:, 1], idx[:, 2]]
+            assert np.abs(got - g["sample_psi"]).max() <= 1e-12 * g["max_abs"][0]
+            assert len(st.checks) == len(g["checks"])
+            for c, want in zip(st.checks, g["checks"]):
+                assert c.step == want[0]
+                assert abs(c.energy - want[1]) <= 1e-10 * abs(want[1])
+                assert abs(c.r_rms - want[3]) <= 1e-10 * abs(want[3])
+            e, r = energy(st.psi, grid), rms_radius(st.psi)
+            assert abs(e - g["final"][0]) <= 1e-10 * abs(g["final"][0])
+            assert abs(r - g["final"][1]) <= 1e-10 * abs(g["final"][1])
+
+
+# ---------------------------------------------------------------- slab engine
+class TestSlabEngine:
+    @pytest.mark.parametrize("workers", [2, 4])
+    def test_bitwise_m_invariance(self, gpu_lib, workers):
+        spec = LatticeSpec(N=16, a=0.5, m=1.0, dtau=0.0625)
+        grid = harmonic(spec)
+        init = fill_random_gaussian(allocate(spec), 7)
+        serial = evolve_to_convergence(init, grid, tol=1e-300, check_freq=25, max_steps=120,
+                                       max_snapshots=0)
+        par = evolve_parallel(grid, workers=workers, initial=init, tol=1e-300, check_freq=25,
+                              max_steps=120, max_snapshots=0)
+        assert np.array_equal(par.psi.values, serial.psi.values)
+        assert [c.energy for c in par.checks] == [c.energy for c in serial.checks]
+        assert [c.r_rms for c in par.checks] == [c.r_rms for c in serial.checks]
+        assert par.halo_messages == 2 * (workers - 1) * 120
+
+    def test_parity_across_slabs(self, gpu_lib):
+        spec = LatticeSpec(N=12, a=0.5, m=1.0, dtau=0.0625)
+        grid = harmonic(spec)
+        init = fill_random_gaussian(allocate(spec), 9)
+        cs = [SymmetryConstraint("x", "antisymmetric"), SymmetryConstraint("z", "symmetric")]
+        for c in cs:
+            impose_inplace(init.values, spec.N, c)
+        serial = evolve_to_convergence(init, grid, tol=1e-300, check_freq=20, max_steps=80,
+                                       constraints=cs, max_snapshots=0)
+        par = evolve_parallel(grid, workers=3, initial=init, tol=1e-300, check_freq=20,
+                              max_steps=80, constraints=cs, max_snapshots=0)
+        assert np.array_equal(par.psi.values, serial.psi.values)

@@ -106,3 +106,14 @@ def test_fixed_run_matches_oracle(gpu_lib, n, steps, check):
         assert abs(e_gpu - e) <= 1e-10 * abs(e)
         rr_gpu = math.sqrt(float(np.sum(sm[2])) / float(np.sum(sm[1])))
         assert abs(rr_gpu - rr) <= 1e-10 * abs(rr)
+
+
+@pytest.mark.parametrize("lo,hi", [(-0.7, 2.9), (-0.76, -0.74), (2.99, 3.01), (-1e-3, 1e-3),
+                                   (-1e-12, 1e-12), (-1e-300, 1e-300), (-1e6, 1e6),
+                                   (-0.999999, -0.99), (0.999, 1.001)])
+def test_coefficient_division_is_ieee(gpu_lib, lo, hi):
+    """The sweep's shared-reciprocal A/B division equals IEEE division bitwise."""
+    import ctypes
+    bad = ctypes.c_uint64()
+    assert gpu_lib.psg_selftest_division(1 << 26, 12345, lo, hi, ctypes.byref(bad)) == 0
+    assert bad.value == 0
