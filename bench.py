@@ -1,0 +1,437 @@
+"""Benchmark of the imaginary-time FDTD hot path (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...   (one rank per GPU)
+
+Workload (BASELINE.json configs[1], "C2"): Coulomb V = -1/max(r, a/2) on a
+256^3 fp64 lattice, a = 0.1, dtau = a*a/4, seeded U(-0.5, 0.5) start
+(synthetic, workloads.py), observables + renormalisation every 500 sweeps.
+A step is one sweep of the whole lattice.  Metric: lattice-site updates per
+second (GLUPS), whole job.  psi (2 buffers) + V are 3 x 137 MB, larger than
+the 126 MB L2, so no flush is needed between steps.
+
+JSON fields beyond the base contract:
+  roofline      dominant kernel (k_sweep) vs measured HBM copy bandwidth:
+                achieved = 24 B/site x N^3 / mean sweep-launch duration
+                (CUDA events on the slab's stream); traffic from the committed
+                ncu capture (profiles/), per launch.
+  cpu_baseline  the CPU oracle port (oracle/, C + OpenMP, all host threads) on
+                a bounded sample of the same workload, rank 0, N=1.
+  e2e           the same metric through the public API (evolve_fixed) from
+                pinned host arrays: upload psi0 + V, K sweeps, download psi
+                and the observable plane sums.
+``--impl reference`` times the reference algorithm's CPU implementation (the
+oracle port: the reference package is Python/numba and cannot be built into
+oracle/_ref) on the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+PEAK_FALLBACK = 6650.0  # GB/s, B200_PROFILING.md fallback when MEASURED_PEAKS.json is absent
+BYTES_PER_SITE = 24     # psi read + V read + psi write, fp64
+
+
+def hbm_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return PEAK_FALLBACK, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        time.sleep(0.25)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        try:
+            for line in open(self.path):
+                f = [x.strip() for x in line.split(",")]
+                if len(f) < 9:
+                    continue
+                try:
+                    sm.append(float(f[1]))
+                    mx = float(f[2])
+                except ValueError:
+                    continue
+                for nm, val in zip(names, f[5:9]):
+                    if val.lower().startswith("active"):
+                        reasons.add(nm)
+        except Exception:
+            pass
+        finally:
+            try:
+                os.unlink(self.path)
+            except Exception:
+                pass
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def load_traffic(n):
+    """dram bytes per sweep launch from the committed ncu capture (or None)."""
+    p = os.path.join(ROOT, "profiles", "sweep_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        rec = d.get(str(n))
+        return float(rec["dram_bytes_per_launch"]) if rec else None
+    except Exception:
+        return None
+
+
+def workload(name="C2"):
+    from paper_0904_0939_b200 import workloads
+
+    return workloads.CONFIGS[name]
+
+
+# ---------------------------------------------------------------------------
+# CPU legs (oracle port) — only place the bench executes oracle/
+# ---------------------------------------------------------------------------
+def cpu_sample(w, target_s=10.0, max_steps=2000):
+    """Time the oracle (C, OpenMP, all host threads) on the workload's fixed-step
+    loop for a bounded number of sweeps; returns (GLUPS, threads, sample)."""
+    from oracle import oracle as O
+    from paper_0904_0939_b200 import workloads
+
+    spec = w.spec
+    n = spec.N
+    psi = np.zeros((n + 2,) * 3)
+    psi[1:-1] = workloads.uniform_start(spec)
+    v = workloads.potential_planes(w, spec, 0, n + 2)
+    out = psi.copy()
+    t0 = time.perf_counter()
+    O.stencil_update_v(psi, v, spec.dtau, spec.m, spec.a, out, 1, n)
+    t1 = time.perf_counter() - t0
+    steps = int(min(max(target_s / max(t1, 1e-6), 3), max_steps))
+    t0 = time.perf_counter()
+    _, checks = O.evolve_fixed(psi, v, n, spec.a, spec.m, spec.dtau, steps, w.measure_every,
+                               norm_every=w.measure_every)
+    dt = time.perf_counter() - t0
+    return (n ** 3 * steps / dt / 1e9, O.threads(),
+            f"{steps} sweeps of the {w.name} lattice ({n}^3), fixed-step loop with "
+            f"norm/measure every {w.measure_every}, oracle/psi_oracle.c with "
+            f"{O.threads()} OpenMP threads")
+
+
+def run_reference(args):
+    """--impl reference: the reference algorithm's CPU implementation (oracle port)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from oracle import oracle as O
+    from paper_0904_0939_b200 import workloads
+
+    w = workload(args.config)
+    spec = w.spec
+    n = spec.N
+    psi = np.zeros((n + 2,) * 3)
+    psi[1:-1] = workloads.uniform_start(spec)
+    v = workloads.potential_planes(w, spec, 0, n + 2)
+    out = psi.copy()
+    # calibrate: keep the whole warmup + steps run within ~3 minutes
+    t0 = time.perf_counter()
+    O.stencil_update_v(psi, v, spec.dtau, spec.m, spec.a, out, 1, n)
+    t1 = time.perf_counter() - t0
+    budget = 150.0
+    planes = n
+    if (args.steps + args.warmup) * t1 > budget:
+        planes = max(1, int(n * budget / ((args.steps + args.warmup) * t1)))
+    a3 = O.cell_volume(spec.a)
+
+    def one(s):
+        nonlocal psi, out
+        O.stencil_update_v(psi, v, spec.dtau, spec.m, spec.a, out, 1, planes)
+        psi, out = out, psi
+        if s % w.measure_every == 0:
+            n2 = O.np_sum(O.norm_plane_sums(psi, 1, n)) * a3
+            O.load().oracle_scale(O._p(psi), psi.size, 1.0 / math.sqrt(n2))
+
+    for s in range(1, args.warmup + 1):
+        one(s)
+    t0 = time.perf_counter()
+    for s in range(args.warmup + 1, args.warmup + args.steps + 1):
+        one(s)
+    dt = time.perf_counter() - t0
+    sites = planes * n * n
+    glups = sites * args.steps / dt / 1e9
+    sample = (f"each step sweeps planes 1..{planes} of the {n}^3 {w.name} lattice "
+              f"({sites} sites) with oracle/psi_oracle.c (C port of the reference kernels, "
+              f"{O.threads()} OpenMP threads)")
+    line = {
+        "metric": "fp64 FDTD lattice-site updates/s (GLUPS)", "value": glups, "unit": "GLUPS",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": w.name, "N": n, "a": spec.a, "dtau": spec.dtau,
+                   "measure_every": w.measure_every},
+        "impl": "reference",
+        "cpu_baseline": {"value": glups, "unit": "GLUPS", "cores": O.threads(), "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": glups, "unit": "GLUPS", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+def _pinned(shape):
+    import torch
+
+    return torch.empty(shape, dtype=torch.float64, pin_memory=True).numpy()
+
+
+def run_single(args):
+    import torch
+
+    from paper_0904_0939_b200 import Field3D, PotentialGrid, evolve_fixed, workloads
+    from paper_0904_0939_b200.device import F_WRITE, Slab
+
+    w = workload(args.config)
+    spec = w.spec
+    n = spec.N
+    ext = n + 2
+    dev = 0
+    torch.cuda.set_device(dev)
+    psi0 = _pinned((ext, ext, ext))
+    psi0[...] = 0.0
+    psi0[1:-1] = workloads.uniform_start(spec)
+    vhost = _pinned((ext, ext, ext))
+    vhost[...] = workloads.potential_planes(w, spec, 0, ext)
+
+    slab = Slab(spec, device=dev)
+    slab.set_field(psi0)
+    slab.set_potential(vhost)
+    st = torch.cuda.ExternalStream(slab.stream)
+    m = w.measure_every
+    slab.run(args.warmup, measure_every=m, norm_every=m)
+    slab.sync()
+
+    # ---- timed region: K sweeps, observables + renormalisation every m ----
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0 = slab.launches()
+    with ClockSampler(dev) as clk:
+        torch.cuda.synchronize()
+        e0.record(st)
+        idx, sums, status = slab.run(args.steps, measure_every=m, norm_every=m,
+                                     step_offset=args.warmup)
+        e1.record(st)
+        e1.synchronize()
+        torch.cuda.synchronize()
+    launches = slab.launches() - l0
+    ms = e0.elapsed_time(e1)
+    clocks = clk.summary()
+    value = n ** 3 * args.steps / (ms * 1e-3) / 1e9
+    if status.any():
+        raise SystemExit(f"device status {status} during the timed run")
+
+    # ---- mean duration of the dominant kernel (sweep launches, same stream) ----
+    reps = 50
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(reps + 1)]
+    evs[0].record(st)
+    for i in range(reps):
+        slab.sweep(1, n, F_WRITE)
+        slab.swap(False)
+        evs[i + 1].record(st)
+    evs[-1].synchronize()
+    durs = [evs[i].elapsed_time(evs[i + 1]) * 1e-3 for i in range(reps)]
+    sweep_s = statistics.mean(durs)
+    slab.close()
+
+    peak, peak_kind = hbm_peak()
+    achieved = BYTES_PER_SITE * n ** 3 / sweep_s / 1e9
+    traffic = load_traffic(n)
+
+    # ---- e2e through the public API from pinned host buffers ----
+    grid = PotentialGrid(spec=spec, v=vhost, v_inf=0.0, unbounded=False, name="custom")
+    init = Field3D(spec, psi0)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    state = evolve_fixed(init, grid, args.steps, m, norm_every=m)
+    t_e2e = time.perf_counter() - t0
+    e2e = n ** 3 * args.steps / t_e2e / 1e9
+    h2d = 2 * ext ** 3 * 8
+    d2h = ext ** 3 * 8 + len(state.checks) * (3 * n + 2) * 8
+
+    cpu = None
+    if not args.no_cpu:
+        g, cores, sample = cpu_sample(w)
+        cpu = {"value": g, "unit": "GLUPS", "cores": cores, "kind": "port", "sample": sample}
+
+    line = {
+        "metric": "fp64 FDTD lattice-site updates/s (GLUPS)",
+        "value": value, "unit": "GLUPS", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": w.name, "N": n, "a": spec.a, "dtau": spec.dtau,
+                   "potential": w.potential, "measure_every": m, "norm_every": m,
+                   "l2": "inputs (3 x %.0f MB) larger than L2; no flush" % (ext ** 3 * 8 / 1e6),
+                   "parallelism": "single GPU"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "k_sweep (fp64 7-point, TMA z-march)",
+                     "kernel_us": sweep_s * 1e6, "peak_source": peak_kind,
+                     "algorithmic_bytes_per_launch": BYTES_PER_SITE * n ** 3},
+        "clocks": clocks,
+        "e2e": {"value": e2e, "unit": "GLUPS", "h2d_bytes_per_step": h2d / args.steps,
+                "d2h_bytes_per_step": d2h / args.steps,
+                "api": "paper_0904_0939_b200.evolve_fixed(Field3D, PotentialGrid) from pinned "
+                       "host memory, psi0+V uploaded and psi downloaded inside the timed region"},
+        "gpu_launches": launches,
+        "cpu_baseline": cpu,
+        "observables": {"E_last": float(np.sum(sums[-1][0]) / np.sum(sums[-1][1]))
+                        if len(sums) else None},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_dist(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_0904_0939_b200 import workloads
+    from paper_0904_0939_b200.device import Slab
+    from paper_0904_0939_b200.parallel import SlabEngine, _DistGroup, partition
+
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    w = workload(args.config)
+    spec = w.spec
+    n = spec.N
+    part = partition(spec, world)
+    lo, hi = part.x_range(rank)
+    slab = Slab(spec, w=part.W, x_lo=lo, device=local)
+    planes = np.zeros((part.W + 2, n + 2, n + 2))
+    planes[1:-1] = workloads.uniform_start(spec, first=lo, count=part.W)
+    slab.set_field(planes)
+    slab.set_potential(workloads.potential_planes(w, spec, lo - 1, part.W + 2))
+
+    class _G:  # the grid object the engine needs (v only used on the host for checks)
+        pass
+
+    grid = _G()
+    grid.spec = spec
+    grid.unbounded = w.potential in ("cornell", "wells")
+    grid.v_inf = 0.0
+    engine = SlabEngine(grid, part, [slab], [rank], _DistGroup(slab, rank, part))
+    m = w.measure_every
+    kw = dict(tol=1e-300, check_freq=m, snap_freq=10 ** 12, reimpose_freq=10 ** 12,
+              max_snapshots=0, constraints=(), norm_every=m, fixed=True, measure_every=m,
+              gather=False)
+    engine.run(max_steps=args.warmup, **kw)
+    st = torch.cuda.ExternalStream(slab.stream)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0 = slab.launches()
+    with ClockSampler(local) as clk:
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0.record(st)
+        engine.run(max_steps=args.steps, **kw)
+        e1.record(st)
+        e1.synchronize()
+        torch.cuda.synchronize()
+        dist.barrier()
+    ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    launches = torch.tensor([float(slab.launches() - l0)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(launches)
+    ms = float(ms.item())
+    value = n ** 3 * args.steps / (ms * 1e-3) / 1e9
+    peak, peak_kind = hbm_peak()
+    if rank == 0:
+        line = {
+            "metric": "fp64 FDTD lattice-site updates/s (GLUPS)", "value": value,
+            "unit": "GLUPS", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": w.name, "N": n, "measure_every": m, "norm_every": m,
+                       "parallelism": f"z-slabs x{world} (NCCL halo + all-reduce)",
+                       "l2": "inputs larger than L2; no flush"},
+            "roofline": {"bound": "hbm", "achieved": BYTES_PER_SITE * n ** 3 * args.steps /
+                         (ms * 1e-3) / 1e9 / world, "peak": peak, "unit": "GB/s",
+                         "frac": BYTES_PER_SITE * n ** 3 * args.steps / (ms * 1e-3) / 1e9 /
+                         world / peak, "traffic": None, "per": "GPU", "peak_source": peak_kind},
+            "clocks": clk.summary(),
+            "e2e": None,
+            "gpu_launches": int(launches.item()),
+            "cpu_baseline": None,
+        }
+        print(json.dumps(line), flush=True)
+    slab.close()
+    dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=4000)
+    ap.add_argument("--warmup", type=int, default=100)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        return run_dist(args)
+    return run_single(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main() or 0)

@@ -229,7 +229,10 @@ class SlabEngine:
     # -- public loop ----------------------------------------------------------
     def run(self, *, tol: float, check_freq: int, snap_freq: int, reimpose_freq: int,
             max_steps: int, max_snapshots: int, constraints: tuple, norm_every: int = 1,
-            fixed: bool = False, measure_every: int | None = None):
+            fixed: bool = False, measure_every: int | None = None, gather: bool = True):
+        """Run max_steps sweeps (evolve_to_convergence semantics unless ``fixed``:
+        then no tracker and no per-step status reads).  Returns (assembled field
+        or None, checks, snapshots, converged, step_count, sweeps started)."""
         spec = self.spec
         a3 = cell_volume(spec)
         dist_mode = isinstance(self.group, _DistGroup)
@@ -297,7 +300,7 @@ class SlabEngine:
                     snaps.append((s_idx * spec.dtau, f))
         converged = converged_at is not None
         step_count = converged_at if converged else max_steps
-        final = self.gather()
+        final = self.gather() if gather else None
         if dist_mode:
             # total over ranks, as reduce_broadcast of the send counters (parallel.py:497)
             import torch
