@@ -272,6 +272,19 @@ class SweepBuffers:
             self._slab = None
 
 
+def _dirichlet_start(initial: Field3D) -> np.ndarray:
+    """The start vector with a zero padding shell (evolve.py:236-238); the
+    caller's array is uploaded as is when its shell is already zero."""
+    v = initial.values
+    shell = (v[0].any() or v[-1].any() or v[:, 0].any() or v[:, -1].any()
+             or v[:, :, 0].any() or v[:, :, -1].any())
+    if not shell:
+        return v
+    start = Field3D(initial.spec, v.copy())
+    apply_dirichlet_boundary(start, 0.0)
+    return start.values
+
+
 def _constraint_pairs(constraints):
     from .states import _AXES
 
@@ -304,13 +317,12 @@ def evolve_to_convergence(initial: Field3D, grid: PotentialGrid, tol: float = 1e
     pairs = _constraint_pairs(constraints)
     tracker = ConvergenceTracker(tol)
 
-    start = Field3D(spec, initial.values.copy())
-    apply_dirichlet_boundary(start, 0.0)
+    start_values = _dirichlet_start(initial)
     slab = Slab(spec)
     snapshots: list = []
     checks: list = []
     try:
-        slab.set_field(start.values)
+        slab.set_field(start_values)
         slab.load_grid(grid)
 
         def finish(step_count: int, converged: bool) -> EvolutionState:
@@ -368,9 +380,7 @@ def evolve_fixed(initial: Field3D, grid: PotentialGrid, steps: int, measure_ever
     own = slab is None
     if own:
         slab = Slab(spec)
-        start = Field3D(spec, initial.values.copy())
-        apply_dirichlet_boundary(start, 0.0)
-        slab.set_field(start.values)
+        slab.set_field(_dirichlet_start(initial))
     slab.load_grid(grid)
     try:
         idx, sums, status = slab.run(steps, measure_every=measure_every, norm_every=norm_every,
