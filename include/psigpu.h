@@ -281,6 +281,19 @@ int psg_run(psg_slab* s, const psg_run_params* p, double* hist, int64_t max_chec
  * (planes per work item), pipeline depth (planes in flight per block: 4/6/8). */
 int psg_tune(psg_slab* s, int blocks_per_sm, int zchunk, int stages);
 
+/* Launch options: 0 = programmatic dependent launch between consecutive
+ * kernels (default 1), 1 = tapered chunk tail (number of chunks re-cut into
+ * quarter-size work items at the end of a sweep, default 0 = off). */
+int psg_set_option(psg_slab* s, int option, int value);
+
+/* Enable / disable (default) two sweeps per pass (temporal blocking) for
+ * pairs of plain steps inside psg_run; results are bitwise unchanged. */
+int psg_set_temporal(psg_slab* s, int enable);
+
+/* Enable / disable (default) the persistent multi-step sweep for runs of
+ * plain steps inside psg_run (cooperative launch, per-tile dataflow flags). */
+int psg_set_march(psg_slab* s, int enable);
+
 /* Number of kernels this slab has launched so far. */
 int64_t psg_launch_count(psg_slab* s);
 

@@ -87,6 +87,24 @@ class Slab:
     def tune(self, blocks_per_sm: int = 0, zchunk: int = 0, stages: int = 0):
         check(self._lib.psg_tune(self._h, blocks_per_sm, zchunk, stages))
 
+    def set_option(self, option: int, value: int):
+        """0: programmatic dependent launch (default 1); 1: tapered chunk tail (default 0)."""
+        check(self._lib.psg_set_option(self._h, option, value))
+
+    def set_pdl(self, value: int):
+        self.set_option(0, value)
+
+    def set_taper(self, value: int):
+        self.set_option(1, value)
+
+    def set_temporal(self, enable: bool):
+        """Two sweeps per HBM pass for pairs of plain steps in run() (default off)."""
+        check(self._lib.psg_set_temporal(self._h, 1 if enable else 0))
+
+    def set_march(self, enable: bool):
+        """Persistent multi-step sweeps for runs of plain steps in run() (default off)."""
+        check(self._lib.psg_set_march(self._h, 1 if enable else 0))
+
     # ------------------------------------------------------------ data
     @property
     def ext(self) -> int:

@@ -117,3 +117,56 @@ def test_coefficient_division_is_ieee(gpu_lib, lo, hi):
     bad = ctypes.c_uint64()
     assert gpu_lib.psg_selftest_division(1 << 26, 12345, lo, hi, ctypes.byref(bad)) == 0
     assert bad.value == 0
+
+
+@pytest.mark.parametrize("n,steps,every", [(16, 50, 0), (40, 123, 20), (64, 300, 100),
+                                           (130, 64, 30)])
+def test_march_matches_single_step_sweeps(gpu_lib, n, steps, every):
+    """The persistent multi-step sweep (dataflow flags across steps) gives the
+    same bits as one launch per sweep, including around norm/measure steps."""
+    spec = LatticeSpec(N=n, a=0.3, m=1.0, dtau=0.3 * 0.3 / 4.0)
+    rng = np.random.default_rng(n)
+    ext = n + 2
+    psi0 = np.zeros((ext,) * 3)
+    psi0[1:-1, 1:-1, 1:-1] = rng.uniform(-0.5, 0.5, (n, n, n))
+    v = np.zeros((ext,) * 3)
+    v[1:-1, 1:-1, 1:-1] = rng.uniform(-1.0, 3.0, (n, n, n))
+    out = []
+    for march in (False, True):
+        with Slab(spec) as s:
+            s.set_march(march)
+            s.set_field(psi0)
+            s.set_potential(v)
+            idx, sums, status = s.run(steps, measure_every=every, norm_every=every)
+            if march:
+                assert s.launches() < steps  # plain steps were batched
+            out.append((s.get_field(), sums))
+    assert np.array_equal(out[0][0], out[1][0])
+    assert np.array_equal(out[0][1], out[1][1])
+
+
+@pytest.mark.parametrize("n,steps,every", [(8, 9, 0), (16, 50, 0), (40, 123, 20), (64, 300, 100),
+                                           (100, 61, 0), (130, 64, 30), (256, 20, 10)])
+def test_two_step_pass_matches_single_steps(gpu_lib, n, steps, every):
+    """Temporal blocking (two sweeps per HBM pass, intermediate plane ring in
+    shared memory) gives the same bits as one launch per sweep."""
+    spec = LatticeSpec(N=n, a=0.3, m=1.0, dtau=0.3 * 0.3 / 4.0)
+    rng = np.random.default_rng(n + 1)
+    ext = n + 2
+    psi0 = np.zeros((ext,) * 3)
+    psi0[1:-1, 1:-1, 1:-1] = rng.uniform(-0.5, 0.5, (n, n, n))
+    v = np.zeros((ext,) * 3)
+    v[1:-1, 1:-1, 1:-1] = rng.uniform(-1.0, 3.0, (n, n, n))
+    out = []
+    for t2 in (False, True):
+        with Slab(spec) as s:
+            s.set_march(False)
+            s.set_temporal(t2)
+            s.set_field(psi0)
+            s.set_potential(v)
+            idx, sums, status = s.run(steps, measure_every=every, norm_every=every)
+            out.append((s.get_field(), sums, s.launches()))
+    assert np.array_equal(out[0][0], out[1][0])
+    assert np.array_equal(out[0][1], out[1][1])
+    if steps > 4:
+        assert out[1][2] < out[0][2]
