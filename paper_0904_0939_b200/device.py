@@ -97,6 +97,9 @@ class Slab:
     def set_taper(self, value: int):
         self.set_option(1, value)
 
+    def set_alt_dir(self, value: int):
+        self.set_option(2, value)
+
     def set_temporal(self, enable: bool):
         """Two sweeps per HBM pass for pairs of plain steps in run() (default off)."""
         check(self._lib.psg_set_temporal(self._h, 1 if enable else 0))
