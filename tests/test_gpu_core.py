@@ -109,13 +109,14 @@ def test_fixed_run_matches_oracle(gpu_lib, n, steps, check):
 
 
 @pytest.mark.parametrize("lo,hi", [(-0.7, 2.9), (-0.76, -0.74), (2.99, 3.01), (-1e-3, 1e-3),
-                                   (-1e-12, 1e-12), (-1e-300, 1e-300), (-1e6, 1e6),
-                                   (-0.999999, -0.99), (0.999, 1.001)])
+                                   (-1e-12, 1e-12), (-1e-15, 1e-15), (-2.3e-16, 2.3e-16),
+                                   (-1e-300, 1e-300), (-1e6, 1e6), (-0.999999, -0.99),
+                                   (0.999, 1.001), (-0.5, -0.4999), (-3e-5, 0.0)])
 def test_coefficient_division_is_ieee(gpu_lib, lo, hi):
     """The sweep's shared-reciprocal A/B division equals IEEE division bitwise."""
     import ctypes
     bad = ctypes.c_uint64()
-    assert gpu_lib.psg_selftest_division(1 << 26, 12345, lo, hi, ctypes.byref(bad)) == 0
+    assert gpu_lib.psg_selftest_division(1 << 28, 12345, lo, hi, ctypes.byref(bad)) == 0
     assert bad.value == 0
 
 
@@ -170,3 +171,21 @@ def test_two_step_pass_matches_single_steps(gpu_lib, n, steps, every):
     assert np.array_equal(out[0][1], out[1][1])
     if steps > 4:
         assert out[1][2] < out[0][2]
+
+
+@pytest.mark.parametrize("n", [12, 64, 100])
+def test_fused_norm_partials_equal_standalone(gpu_lib, n):
+    """The sweep's fused NORM partials and the standalone norm pass of the
+    stored output reduce in the same fixed order: identical plane sums."""
+    spec, psi, v = _case(n, 500 + n)
+    with Slab(spec) as s:
+        s.set_field(psi)
+        s.set_potential(v)
+        s.sweep(1, n, F_WRITE | F_NORM)
+        s.reduce(1, n, F_NORM, combine=False)
+        fused = s.read_sums()[0][3].copy()
+        s.swap()
+        s.norm_partials()
+        s.reduce(1, n, F_NORM, combine=False)
+        alone = s.read_sums()[0][3].copy()
+    assert np.array_equal(fused, alone)
