@@ -54,6 +54,7 @@ extern "C" {
 #define PSG_F_WRITE 1u   /* update psi (stencil_update) */
 #define PSG_F_NORM 2u    /* per-plane sum of out^2 (norm_plane_sums on the output) */
 #define PSG_F_MEASURE 4u /* per-plane num/den/r2 on the input (energy_ + radius2_plane_sums) */
+#define PSG_F_CHECK 8u   /* flag non-finite outputs (evolve.step's isfinite check, evolve.py:49-52) */
 
 /* reduction quantity slots in the plane-sum vectors */
 #define PSG_Q_NUM 0

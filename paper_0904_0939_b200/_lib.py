@@ -22,6 +22,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 F_WRITE = 1
 F_NORM = 2
 F_MEASURE = 4
+F_CHECK = 8
 Q_NUM, Q_DEN, Q_R2, Q_NORM = 0, 1, 2, 3
 
 # scalar slots filled by psg_read_sums (include/psigpu.h)

@@ -13,11 +13,11 @@ import ctypes
 import numpy as np
 
 from . import _lib
-from ._lib import F_MEASURE, F_NORM, F_WRITE, NSCAL, RunParams, check, dptr, lptr
+from ._lib import F_CHECK, F_MEASURE, F_NORM, F_WRITE, NSCAL, RunParams, check, dptr, lptr
 from .errors import ConfigError, DeviceError, SingularCoefficientError
 from .lattice import LatticeSpec
 
-__all__ = ["Slab", "F_WRITE", "F_NORM", "F_MEASURE"]
+__all__ = ["Slab", "F_WRITE", "F_NORM", "F_MEASURE", "F_CHECK"]
 
 
 class _DeviceArray:
@@ -103,6 +103,10 @@ class Slab:
     def set_temporal(self, enable: bool):
         """Two sweeps per HBM pass for pairs of plain steps in run() (default off)."""
         check(self._lib.psg_set_temporal(self._h, 1 if enable else 0))
+
+    def set_zchunk(self, zc: int):
+        """Planes per work item of the sweep (0 = automatic)."""
+        self.tune(0, zc, 0)
 
     def set_march(self, enable: bool):
         """Persistent multi-step sweeps for runs of plain steps in run() (default off)."""

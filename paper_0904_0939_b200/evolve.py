@@ -20,7 +20,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from ._lib import F_NORM, F_WRITE
+from ._lib import F_CHECK, F_NORM, F_WRITE
 from .errors import ConfigError, DivergenceError, ZeroNormError
 from .lattice import Field3D, LatticeSpec, apply_dirichlet_boundary
 from .observables import (cell_volume, combine_plane_sums, measure_device)
@@ -70,7 +70,7 @@ def step(psi: Field3D, grid: PotentialGrid) -> Field3D:
     with Slab(psi.spec) as s:
         s.set_field(psi.values)
         s.load_grid(grid)
-        s.sweep(1, psi.spec.N, F_WRITE)
+        s.sweep(1, psi.spec.N, F_WRITE | F_CHECK)
         s.swap()
         out = s.get_field()
         bad = s.read_sums()[1][12]

@@ -115,9 +115,10 @@ def test_fixed_run_matches_oracle(gpu_lib, n, steps, check):
 def test_coefficient_division_is_ieee(gpu_lib, lo, hi):
     """The sweep's shared-reciprocal A/B division equals IEEE division bitwise."""
     import ctypes
-    bad = ctypes.c_uint64()
-    assert gpu_lib.psg_selftest_division(1 << 28, 12345, lo, hi, ctypes.byref(bad)) == 0
-    assert bad.value == 0
+    for count in (1 << 28, -(1 << 28)):   # per-site path, and the warp-uniform fast path
+        bad = ctypes.c_uint64()
+        assert gpu_lib.psg_selftest_division(count, 12345, lo, hi, ctypes.byref(bad)) == 0
+        assert bad.value == 0
 
 
 @pytest.mark.parametrize("n,steps,every", [(16, 50, 0), (40, 123, 20), (64, 300, 100),
