@@ -488,3 +488,23 @@ class TestSlabEngine:
         par = evolve_parallel(grid, workers=3, initial=init, tol=1e-300, check_freq=20,
                               max_steps=80, constraints=cs, max_snapshots=0)
         assert np.array_equal(par.psi.values, serial.psi.values)
+
+
+def test_nccl_slab_path_single_rank(gpu_lib):
+    """The torch.distributed (NCCL) slab engine on one real GPU under torchrun:
+    device plane views, NCCL all-reduce on the slab stream, gather; bitwise
+    equal to the single-slab run (multi-rank P2P is covered over gloo)."""
+    import socket
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with socket.socket() as sck:
+        sck.bind(("127.0.0.1", 0))
+        port = sck.getsockname()[1]
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        "--nproc-per-node", "1", "--master-addr", "127.0.0.1", "--master-port",
+                        str(port), os.path.join(root, "scripts", "dist_smoke.py")],
+                       cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
+    assert "psi bitwise True" in r.stdout and "energies bitwise True" in r.stdout
