@@ -289,8 +289,9 @@ int psg_tune(psg_slab* s, int blocks_per_sm, int zchunk, int stages);
  * its predecessor wrote last, still in L2 (default 1; bitwise unchanged). */
 int psg_set_option(psg_slab* s, int option, int value);
 
-/* Enable / disable (default) two sweeps per pass (temporal blocking) for
- * pairs of plain steps inside psg_run; results are bitwise unchanged. */
+/* Enable / disable two sweeps per HBM pass (temporal blocking) for pairs of
+ * plain steps inside psg_run; default on for N >= 288 (measured crossover);
+ * results are bitwise unchanged. */
 int psg_set_temporal(psg_slab* s, int enable);
 
 /* Enable / disable (default) the persistent multi-step sweep for runs of

@@ -101,7 +101,7 @@ class Slab:
         self.set_option(2, value)
 
     def set_temporal(self, enable: bool):
-        """Two sweeps per HBM pass for pairs of plain steps in run() (default off)."""
+        """Two sweeps per HBM pass for pairs of plain steps in run() (default: N >= 288)."""
         check(self._lib.psg_set_temporal(self._h, 1 if enable else 0))
 
     def set_zchunk(self, zc: int):

@@ -49,7 +49,7 @@ print(json.dumps(res))
 
 
 def run(names, ns, reps, opts):
-    steps = {64: 4000, 128: 3000, 256: 1500, 512: 300, 1024: 40}
+    steps = {n: max(40, min(4000, int(2.5e10 / n ** 3))) for n in ns}
     table = {nm: {n: [] for n in ns} for nm in names}
     for r in range(reps):
         for nm in names:
