@@ -286,7 +286,9 @@ int psg_tune(psg_slab* s, int blocks_per_sm, int zchunk, int stages);
  * kernels (default 1), 1 = tapered chunk tail (number of chunks re-cut into
  * quarter-size work items at the end of a sweep, default 0 = off), 2 =
  * alternate the z-march direction every sweep so a sweep starts on the planes
- * its predecessor wrote last, still in L2 (default 1; bitwise unchanged). */
+ * its predecessor wrote last, still in L2 (default 1; bitwise unchanged),
+ * 3 = tile rows of the two-sweep pass, 8 (two blocks per SM) or 16 (one
+ * block per SM, default; bitwise unchanged). */
 int psg_set_option(psg_slab* s, int option, int value);
 
 /* Enable / disable two sweeps per HBM pass (temporal blocking) for pairs of

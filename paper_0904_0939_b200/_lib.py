@@ -17,7 +17,9 @@ from ctypes import POINTER, c_double, c_int, c_int32, c_int64, c_uint, c_void_p
 from .errors import raise_for_status
 
 LIB_NAME = "libpsigpu.so"
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+# PSG_LIB overrides the in-tree library (developer A/B builds)
+LIB_PATH = os.environ.get("PSG_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                                     LIB_NAME)
 
 F_WRITE = 1
 F_NORM = 2

@@ -100,8 +100,12 @@ class Slab:
     def set_alt_dir(self, value: int):
         self.set_option(2, value)
 
+    def set_t2_rows(self, rows: int):
+        """Tile rows of the two-sweep pass: 8 or 16 (default)."""
+        self.set_option(3, rows)
+
     def set_temporal(self, enable: bool):
-        """Two sweeps per HBM pass for pairs of plain steps in run() (default: N >= 288)."""
+        """Two sweeps per HBM pass for pairs of plain steps in run() (default: N >= 96)."""
         check(self._lib.psg_set_temporal(self._h, 1 if enable else 0))
 
     def set_zchunk(self, zc: int):

@@ -16,10 +16,15 @@ ABDIR = os.path.join(HERE, "ab")
 
 def build(name, flags):
     os.makedirs(ABDIR, exist_ok=True)
+    src = os.path.join(ROOT, "paper_0904_0939_b200", "csrc", "psigpu.cu")
+    for f in list(flags):
+        if f.startswith("--src="):
+            src = f[len("--src="):]
+            flags.remove(f)
     out = os.path.join(ABDIR, f"libpsigpu_{name}.so")
     cmd = ["/usr/local/cuda/bin/nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3",
            "-lineinfo", "--fmad=false", "-std=c++17", *flags, "-Xcompiler", "-fPIC", "-shared",
-           "-cudart", "static", "-o", out, os.path.join(ROOT, "paper_0904_0939_b200", "csrc", "psigpu.cu")]
+           "-cudart", "static", "-I", os.path.join(ROOT, "include"), "-o", out, src]
     subprocess.run(cmd, check=True)
     print(out)
 

@@ -37,6 +37,19 @@ KEYS = [
     "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio",
     "smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio",
     "smsp__average_warps_issue_stalled_branch_resolving_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_mio_throttle_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_math_pipe_throttle_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_not_selected_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_no_instruction_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_dispatch_stall_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_lg_throttle_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_sleeping_per_issue_active.ratio",
+    "smsp__issue_active.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed.avg.per_cycle_active",
+    "smsp__inst_executed.sum",
+    "sm__cycles_elapsed.avg.per_second",
+    "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
 ]
 
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
@@ -79,13 +92,15 @@ def full(rep, label, n=None):
     for rec in out:
         print(json.dumps({k: rec[k] for k in rec if not k.endswith(".unit")}))
     if n is not None and out:
-        tpath = os.path.join(PROF, "sweep_traffic.json")
+        first = out[0]
+        kname = "k_sweep2b" if "k_sweep2b" in first["kernel"] else "k_sweep"
+        tpath = os.path.join(PROF, "sweep_traffic.json" if kname == "k_sweep"
+                             else f"{kname}_traffic.json")
         try:
             with open(tpath) as f:
                 tr = json.load(f)
         except Exception:
             tr = {}
-        first = out[0]
         tr[str(n)] = {"dram_bytes_per_launch": first["dram_bytes_per_launch"],
                       "duration_s": first.get("gpu__time_duration.sum"),
                       "kernel": first["kernel"], "source": f"profiles/ncu_{label}.json",

@@ -52,6 +52,9 @@ if __name__ == "__main__":
     if mode == "profile":
         n, steps, norm, meas = (int(x) for x in sys.argv[2:6])
         s = make(n)
+        if len(sys.argv) > 6:
+            s.set_temporal(True)
+            s.set_t2_rows(int(sys.argv[6]))
         timed(s, n, steps, norm, meas)
         sys.exit(0)
     for n in (256, 512):

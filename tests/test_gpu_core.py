@@ -149,7 +149,8 @@ def test_march_matches_single_step_sweeps(gpu_lib, n, steps, every):
 
 @pytest.mark.parametrize("n,steps,every", [(8, 9, 0), (16, 50, 0), (40, 123, 20), (64, 300, 100),
                                            (100, 61, 0), (130, 64, 30), (256, 20, 10)])
-def test_two_step_pass_matches_single_steps(gpu_lib, n, steps, every):
+@pytest.mark.parametrize("rows", [8, 16])
+def test_two_step_pass_matches_single_steps(gpu_lib, n, steps, every, rows):
     """Temporal blocking (two sweeps per HBM pass, intermediate plane ring in
     shared memory) gives the same bits as one launch per sweep."""
     spec = LatticeSpec(N=n, a=0.3, m=1.0, dtau=0.3 * 0.3 / 4.0)
@@ -164,6 +165,7 @@ def test_two_step_pass_matches_single_steps(gpu_lib, n, steps, every):
         with Slab(spec) as s:
             s.set_march(False)
             s.set_temporal(t2)
+            s.set_t2_rows(rows)
             s.set_field(psi0)
             s.set_potential(v)
             idx, sums, status = s.run(steps, measure_every=every, norm_every=every)
@@ -172,6 +174,40 @@ def test_two_step_pass_matches_single_steps(gpu_lib, n, steps, every):
     assert np.array_equal(out[0][1], out[1][1])
     if steps > 4:
         assert out[1][2] < out[0][2]
+
+
+@pytest.mark.parametrize("n,rows,wide,force", [(40, 16, False, True), (72, 16, True, False),
+                                               (72, 8, True, False), (130, 16, True, True)])
+def test_two_step_pass_coefficient_paths(gpu_lib, n, rows, wide, force):
+    """The two-step pass's coefficient paths: without the per-plane range vote
+    (every d = 1 + hV in [0.25, 4), checked at upload), with it (option 4),
+    and potentials reaching d >= 4 or d < 0.25 (IEEE division per site) all
+    give the bits of one launch per sweep."""
+    spec = LatticeSpec(N=n, a=0.3, m=1.0, dtau=0.3 * 0.3 / 4.0)
+    rng = np.random.default_rng(7 * n)
+    ext = n + 2
+    psi0 = np.zeros((ext,) * 3)
+    psi0[1:-1, 1:-1, 1:-1] = rng.uniform(-0.5, 0.5, (n, n, n))
+    v = np.zeros((ext,) * 3)
+    v[1:-1, 1:-1, 1:-1] = rng.uniform(-1.0, 3.0, (n, n, n))
+    if wide:
+        h = spec.dtau / 2
+        # a few planes with d far outside [0.25, 4) on both sides (|psi| still bounded)
+        v[n // 3, 1:-1, 1:-1] = rng.uniform(4.0 / h, 9.0 / h, (n, n))
+        v[n // 2, 1:-1, 1:-1] = rng.uniform(-0.9 / h, -0.8 / h, (n, n))
+    out = []
+    for t2 in (False, True):
+        with Slab(spec) as s:
+            s.set_march(False)
+            s.set_temporal(t2)
+            s.set_t2_rows(rows)
+            s.set_option(4, 1 if force else 0)
+            s.set_field(psi0)
+            s.set_potential(v)
+            idx, sums, status = s.run(40, measure_every=20, norm_every=20)
+            out.append((s.get_field(), sums))
+    assert np.array_equal(out[0][0], out[1][0])
+    assert np.array_equal(out[0][1], out[1][1])
 
 
 @pytest.mark.parametrize("n", [12, 64, 100])
