@@ -321,7 +321,7 @@ def run_single(args):
     grid = PotentialGrid(spec=spec, v=vhost, v_inf=0.0, unbounded=False, name="custom")
     init = Field3D(spec, psi0)
     e2e_times = []
-    for _ in range(3):   # the user-facing call, from host arrays, median of three
+    for _ in range(5):   # the user-facing call, from host arrays, median of five
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         state = evolve_fixed(init, grid, args.steps, m, norm_every=m)
@@ -356,7 +356,7 @@ def run_single(args):
                 "d2h_bytes_per_step": d2h / args.steps,
                 "api": "paper_0904_0939_b200.evolve_fixed(Field3D, PotentialGrid) from pinned "
                        "host memory, psi0+V uploaded and psi downloaded inside the timed region",
-                "calls_s": [round(t, 4) for t in e2e_times], "statistic": "median of 3 calls"},
+                "calls_s": [round(t, 4) for t in e2e_times], "statistic": "median of 5 calls"},
         "gpu_launches": launches,
         "cpu_baseline": cpu,
         "observables": {"E_last": float(np.sum(sums[-1][0]) / np.sum(sums[-1][1]))

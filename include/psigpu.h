@@ -78,6 +78,11 @@ int psg_device_count(void);
  * pitch (doubles) for a lattice of n interior sites per axis. */
 int64_t psg_row_pitch(int64_t n);
 
+/* Slab fields come from the device's stream-ordered memory pool and go back
+ * to it on psg_destroy (cached for the next slab of the process); this
+ * returns the cached memory of `device` to the driver. */
+int psg_trim_memory(int device);
+
 /* numpy.sum replica (pairwise, 8 accumulators, 128 blocks) on the device:
  * replaces observables.combine_plane_sums (observables.py:32-34) where the
  * combine must happen without a host round trip.  out[0] = sum(a[0..n)). */

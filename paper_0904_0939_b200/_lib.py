@@ -55,6 +55,7 @@ SIGNATURES = {
     "psg_last_error": (ctypes.c_char_p, []),
     "psg_device_count": (c_int, []),
     "psg_row_pitch": (c_int64, [c_int64]),
+    "psg_trim_memory": (c_int, [c_int]),
     "psg_pairwise_sum_device": (c_int, [_dp, c_int64, _dp]),
     "psg_selftest_division": (c_int, [c_int64, ctypes.c_uint64, c_double, c_double,
                                       POINTER(ctypes.c_uint64)]),

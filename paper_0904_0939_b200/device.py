@@ -100,6 +100,14 @@ class Slab:
     def set_alt_dir(self, value: int):
         self.set_option(2, value)
 
+    def set_t2_stages(self, stages: int):
+        """TMA pipeline depth of the 16-row two-sweep pass: 6 or 9."""
+        self.set_option(5, stages)
+
+    def set_coef_check(self, on: int):
+        """Always take the range-checked coefficient path (default: only when needed)."""
+        self.set_option(4, on)
+
     def set_t2_rows(self, rows: int):
         """Tile rows of the two-sweep pass: 8 or 16 (default)."""
         self.set_option(3, rows)
