@@ -134,6 +134,7 @@ int psg_kernel_dot_plane_sums(const double* psi1, const double* psi2, int64_t pl
 /* ------------------------------------------------------------------ */
 
 typedef struct psg_slab psg_slab;
+typedef struct psg_comm psg_comm;
 
 /* Create a slab on `device` for a lattice (N=n, a, m, dtau) owning the
  * global interior planes x_lo..x_lo+w-1 (1-based; w=n for one GPU).
@@ -282,6 +283,45 @@ typedef struct psg_run_params {
  * (num | den | r2).  max_checks bounds the history. */
 int psg_run(psg_slab* s, const psg_run_params* p, double* hist, int64_t max_checks,
             int64_t* n_checks);
+
+/* --- multi-GPU (z-slabs, one process per GPU; parallel.py:413-485) ------
+ * NCCL is loaded at run time (libnccl.so.2; the one PyTorch loaded when
+ * present).  The 128-byte unique id of rank 0 reaches the other ranks through
+ * the caller's own channel (torch.distributed broadcast). */
+int psg_nccl_available(void);
+int psg_nccl_unique_id(void* out128);
+int psg_comm_create(int device, int nranks, int rank, const void* unique_id128, psg_comm** out);
+int psg_comm_destroy(psg_comm* c);
+/* planes sent by this rank so far (the reference's halo message counter) */
+int64_t psg_comm_halo_messages(psg_comm* c);
+
+/* psg_run for one slab of a z-decomposed lattice (the slab worker loop of
+ * parallel.py:413-485 without host round trips): every sweep posts the
+ * edge-plane send/recv to the neighbour ranks (left / right, -1 = lattice
+ * boundary) on a communication stream, sweeps the interior planes meanwhile,
+ * then the edge planes; reductions go into the zero-padded global plane-sum
+ * vector, NCCL all-reduce (exact: one non-zero contributor per slot), combine
+ * on the device; the factor is folded into the next sweep.  Bitwise equal to
+ * the single-slab run for any slab count.  Parity constraints along the slab
+ * axis are not supported here (PSG_ERR_CONFIG; the Python engine's mirror
+ * exchange handles them). */
+int psg_run_dist(psg_slab* s, psg_comm* c, int left, int right, const psg_run_params* p,
+                 double* hist, int64_t max_checks, int64_t* n_checks);
+
+/* psg_run for m slabs tiling one lattice in order (x_lo = 1, 1+W0, ...),
+ * driven by this process: halos move by peer copies (cudaMemcpyPeerAsync:
+ * NVLink between GPUs, a plain copy on one device), overlapped with the
+ * interior updates; pairs of plain steps use two-sweep passes with two halo
+ * planes per face.  Slabs may live on different devices.  Bitwise equal to
+ * the single-slab run.  hist receives the records of slabs[0]. */
+int psg_run_multi(psg_slab** slabs, int m, const psg_run_params* p, double* hist,
+                  int64_t max_checks, int64_t* n_checks);
+
+/* Observables of the slab's current state (halo exchange, measuring pass,
+ * all-reduce, combine), as one history record of psg_run (3n+2 doubles). */
+int psg_measure_dist(psg_slab* s, psg_comm* c, int left, int right, double* rec);
+/* The same for m slabs driven by this process (psg_run_multi's transport). */
+int psg_measure_multi(psg_slab** slabs, int m, double* rec);
 
 /* Kernel tuning knobs (0 = automatic): sweep blocks per SM, z-chunk length
  * (planes per work item), pipeline depth (planes in flight per block: 4/6/8). */

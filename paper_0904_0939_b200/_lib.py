@@ -92,6 +92,16 @@ SIGNATURES = {
     "psg_impose": (c_int, [c_void_p, c_int, c_int, c_int]),
     "psg_resample": (c_int, [c_void_p, c_void_p, _lp, _dp]),
     "psg_run": (c_int, [c_void_p, POINTER(RunParams), _dp, c_int64, _lp]),
+    "psg_nccl_available": (c_int, []),
+    "psg_nccl_unique_id": (c_int, [c_void_p]),
+    "psg_comm_create": (c_int, [c_int, c_int, c_int, c_void_p, POINTER(c_void_p)]),
+    "psg_comm_destroy": (c_int, [c_void_p]),
+    "psg_comm_halo_messages": (c_int64, [c_void_p]),
+    "psg_run_dist": (c_int, [c_void_p, c_void_p, c_int, c_int, POINTER(RunParams), _dp, c_int64,
+                             _lp]),
+    "psg_measure_dist": (c_int, [c_void_p, c_void_p, c_int, c_int, _dp]),
+    "psg_run_multi": (c_int, [POINTER(c_void_p), c_int, POINTER(RunParams), _dp, c_int64, _lp]),
+    "psg_measure_multi": (c_int, [POINTER(c_void_p), c_int, _dp]),
     "psg_tune": (c_int, [c_void_p, c_int, c_int, c_int]),
     "psg_norm_partials": (c_int, [c_void_p, c_int64, c_int64]),
     "psg_use_factor": (c_int, [c_void_p]),

@@ -272,14 +272,8 @@ class Slab:
         frac = np.ascontiguousarray(frac, dtype=np.float64)
         check(self._lib.psg_resample(coarse._h, self._h, lptr(i0), dptr(frac)))
 
-    def run(self, steps: int, measure_every: int = 0, norm_every: int = 1,
-            reimpose_every: int = 0, constraints=(), step_offset: int = 0,
-            max_checks: int | None = None):
-        """Fused fixed-step driver (psg_run).
-
-        constraints: sequence of (storage axis, sign) applied in order every
-        reimpose_every sweeps.  Returns (state indices, plane sums [c, 3, N]
-        as num|den|r2, per-check status)."""
+    def _run_params(self, steps, measure_every, norm_every, reimpose_every, constraints,
+                    step_offset, max_checks):
         constraints = list(constraints)
         if len(constraints) > 3:
             raise ConfigError("at most 3 parity constraints")
@@ -289,14 +283,122 @@ class Slab:
                       len(constraints), axes, signs, 0)
         if max_checks is None:
             max_checks = steps // measure_every + 1 if measure_every > 0 else 0
-        rec = 3 * self.n + 2
-        hist = np.zeros((max(max_checks, 1), rec))
-        nc = ctypes.c_int64()
-        check(self._lib.psg_run(self._h, ctypes.byref(p), dptr(hist), max_checks, ctypes.byref(nc)))
-        hist = hist[:nc.value]
+        hist = np.zeros((max(max_checks, 1), 3 * self.n + 2))
+        return p, max_checks, hist
+
+    def _unpack_hist(self, hist, nc):
+        hist = hist[:nc]
         return (hist[:, 0].astype(np.int64), hist[:, 2:].reshape(-1, 3, self.n),
                 hist[:, 1].astype(np.int64))
+
+    def run(self, steps: int, measure_every: int = 0, norm_every: int = 1,
+            reimpose_every: int = 0, constraints=(), step_offset: int = 0,
+            max_checks: int | None = None):
+        """Fused fixed-step driver (psg_run).
+
+        constraints: sequence of (storage axis, sign) applied in order every
+        reimpose_every sweeps.  Returns (state indices, plane sums [c, 3, N]
+        as num|den|r2, per-check status)."""
+        p, max_checks, hist = self._run_params(steps, measure_every, norm_every, reimpose_every,
+                                               constraints, step_offset, max_checks)
+        nc = ctypes.c_int64()
+        check(self._lib.psg_run(self._h, ctypes.byref(p), dptr(hist), max_checks, ctypes.byref(nc)))
+        return self._unpack_hist(hist, nc.value)
+
+    def run_dist(self, comm: "Comm", left: int | None, right: int | None, steps: int,
+                 measure_every: int = 0, norm_every: int = 1, reimpose_every: int = 0,
+                 constraints=(), step_offset: int = 0, max_checks: int | None = None):
+        """psg_run for one slab of a z-decomposed lattice: NCCL halo exchange
+        overlapped with the interior sweep, all-reduced plane sums, no host
+        round trips (psg_run_dist).  left / right: neighbour ranks or None."""
+        p, max_checks, hist = self._run_params(steps, measure_every, norm_every, reimpose_every,
+                                               constraints, step_offset, max_checks)
+        nc = ctypes.c_int64()
+        check(self._lib.psg_run_dist(self._h, comm.handle, -1 if left is None else int(left),
+                                     -1 if right is None else int(right), ctypes.byref(p),
+                                     dptr(hist), max_checks, ctypes.byref(nc)))
+        return self._unpack_hist(hist, nc.value)
+
+    def measure_dist(self, comm: "Comm", left: int | None, right: int | None):
+        """Plane sums (3, N) of the current state of a slab of a z-decomposed
+        lattice, all-reduced over the ranks (psg_measure_dist)."""
+        rec = np.zeros(3 * self.n + 2)
+        check(self._lib.psg_measure_dist(self._h, comm.handle, -1 if left is None else int(left),
+                                         -1 if right is None else int(right), dptr(rec)))
+        return rec[2:].reshape(3, self.n)
 
     def status(self) -> int:
         """Sticky device status: 0 ok, 3 zero norm, 4 non-finite (read_sums scal[9])."""
         return int(self.read_sums()[1][9])
+
+
+def run_multi(slabs, steps: int, measure_every: int = 0, norm_every: int = 1,
+              reimpose_every: int = 0, constraints=(), step_offset: int = 0,
+              max_checks: int | None = None):
+    """psg_run over slabs tiling one lattice, driven by this process (peer
+    copies for the halos; slabs may live on different GPUs)."""
+    s0 = slabs[0]
+    p, max_checks, hist = s0._run_params(steps, measure_every, norm_every, reimpose_every,
+                                         constraints, step_offset, max_checks)
+    arr = (ctypes.c_void_p * len(slabs))(*[sl._h for sl in slabs])
+    nc = ctypes.c_int64()
+    check(s0._lib.psg_run_multi(arr, len(slabs), ctypes.byref(p), dptr(hist), max_checks,
+                                ctypes.byref(nc)))
+    return s0._unpack_hist(hist, nc.value)
+
+
+def measure_multi(slabs):
+    """Plane sums (3, N) of the current state of slabs tiling one lattice."""
+    s0 = slabs[0]
+    rec = np.zeros(3 * s0.n + 2)
+    arr = (ctypes.c_void_p * len(slabs))(*[sl._h for sl in slabs])
+    check(s0._lib.psg_measure_multi(arr, len(slabs), dptr(rec)))
+    return rec[2:].reshape(3, s0.n)
+
+
+class Comm:
+    """NCCL communicator of the native multi-GPU run (psg_comm_create).
+
+    Rank 0 draws the NCCL unique id; it reaches the other ranks through
+    torch.distributed (the process group the launcher set up)."""
+
+    def __init__(self, device: int, rank: int, world: int, unique_id: bytes):
+        self._lib = _lib.load()
+        if len(unique_id) != 128:
+            raise ConfigError("NCCL unique id must be 128 bytes")
+        buf = ctypes.create_string_buffer(unique_id, 128)
+        h = ctypes.c_void_p()
+        check(self._lib.psg_comm_create(device, world, rank, buf, ctypes.byref(h)))
+        self.handle = h
+        self.rank, self.world, self.device = rank, world, device
+
+    @staticmethod
+    def unique_id() -> bytes:
+        lib = _lib.load()
+        buf = ctypes.create_string_buffer(128)
+        check(lib.psg_nccl_unique_id(buf))
+        return buf.raw
+
+    @classmethod
+    def from_process_group(cls, device: int):
+        """Build the communicator over the ranks of the default torch process group."""
+        import torch.distributed as dist
+
+        rank, world = dist.get_rank(), dist.get_world_size()
+        obj = [cls.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        return cls(device, rank, world, obj[0])
+
+    def halo_messages(self) -> int:
+        return int(self._lib.psg_comm_halo_messages(self.handle))
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self._lib.psg_comm_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

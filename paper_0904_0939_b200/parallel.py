@@ -117,10 +117,12 @@ def scaling_estimate(dtu: float, dtc: float, n: int, m: int) -> ScalingEstimate:
 # communicators
 # ---------------------------------------------------------------------------
 class _LocalGroup:
-    """All slabs driven by this process (transport "inproc")."""
+    """All slabs driven by this process (transport "inproc").  ``native``:
+    runs go through the library's multi-slab loop (psg_run_multi)."""
 
-    def __init__(self, slabs):
+    def __init__(self, slabs, native: bool = False):
         self.slabs = slabs
+        self.native = native
 
     def exchange_halos(self):
         sl = self.slabs
@@ -142,13 +144,14 @@ class _DistGroup:
     """One slab per process over torch.distributed (NCCL for GPUs, gloo for
     the CPU test slabs)."""
 
-    def __init__(self, slab, rank: int, part: SlabPartition):
+    def __init__(self, slab, rank: int, part: SlabPartition, comm=None):
         import torch.distributed as dist
 
         self.dist = dist
         self.slab = slab
         self.rank = rank
         self.part = part
+        self.comm = comm   # device.Comm: native NCCL run loop (psg_run_dist)
 
     def post_halos(self):
         dist = self.dist
@@ -236,6 +239,14 @@ class SlabEngine:
         spec = self.spec
         a3 = cell_volume(spec)
         dist_mode = isinstance(self.group, _DistGroup)
+        native_ok = (self.group.comm is not None if dist_mode else
+                     getattr(self.group, "native", False))
+        if native_ok and not any(_axis_of(c) == 0 for c in constraints):
+            return self._run_native(tol=tol, check_freq=check_freq, snap_freq=snap_freq,
+                                    reimpose_freq=reimpose_freq, max_steps=max_steps,
+                                    max_snapshots=max_snapshots, constraints=constraints,
+                                    norm_every=norm_every, fixed=fixed,
+                                    measure_every=measure_every, gather=gather)
         stab = check_stability(spec)
         tracker = None if fixed else ConvergenceTracker(tol)
         measure_every = check_freq if measure_every is None else measure_every
@@ -310,6 +321,113 @@ class SlabEngine:
             self.group.dist.all_reduce(t)
             self.halo_messages = int(t.item())
         return final, checks, snaps, converged, step_count, s_idx
+
+    def _run_native(self, *, tol, check_freq, snap_freq, reimpose_freq, max_steps,
+                    max_snapshots, constraints, norm_every, fixed, measure_every, gather):
+        """dist mode over the native loop (psg_run_dist): the sweeps between two
+        host events run on the device with NCCL halos and all-reduces, no
+        per-sweep Python.  Host events: the sweep that measures a check (when
+        a tracker decides), snapshots, the end.  Same sweep / check / snapshot
+        sequence as the per-step loop above."""
+        from .states import _AXES
+
+        from .device import measure_multi, run_multi
+
+        spec = self.spec
+        s = self.slabs[0]
+        dist_mode = isinstance(self.group, _DistGroup)
+        if dist_mode:
+            rank = self.ranks[0]
+            comm = self.group.comm
+            left, right = self.part.left(rank), self.part.right(rank)
+
+            def nrun(nsteps, **kw):
+                return s.run_dist(comm, left, right, nsteps, **kw)
+
+            def nmeasure():
+                return s.measure_dist(comm, left, right)
+
+            def nstatus():
+                return s.status()
+        else:
+            def nrun(nsteps, **kw):
+                return run_multi(self.slabs, nsteps, **kw)
+
+            def nmeasure():
+                return measure_multi(self.slabs)
+
+            def nstatus():
+                codes = [sl.status() for sl in self.slabs]
+                return max(codes)
+        stab = check_stability(spec)
+        tracker = None if fixed else ConvergenceTracker(tol)
+        m = check_freq if measure_every is None else measure_every
+        pairs = [(_AXES[c.axis], int(c.sign)) for c in constraints]
+        checks, snaps = [], []
+        converged_at = None
+        h0 = comm.halo_messages() if dist_mode else 0
+        done = 0
+        started = 0
+        next_check = m                          # state index of the next tracked check
+        fused_m = m if tracker is None else 0   # fixed runs measure inside the loop
+        while done < max_steps:
+            # next host event (sweeps completed): the end, a snapshot, a check the
+            # tracker decides on (state index c, measured before sweep c+1)
+            nxt = max_steps
+            if len(snaps) < max_snapshots:
+                nxt = min(nxt, (done // snap_freq + 1) * snap_freq)
+            if tracker is not None and m > 0:
+                nxt = min(nxt, next_check)
+            if nxt > done:
+                idx, sums, _ = nrun(nxt - done, measure_every=fused_m, norm_every=norm_every,
+                                    reimpose_every=reimpose_freq if pairs else 0,
+                                    constraints=pairs, step_offset=done)
+                if not dist_mode:
+                    self.halo_messages += 2 * (len(self.slabs) - 1) * (nxt - done)
+                done = nxt
+                for st, sm in zip(idx, sums):
+                    rec = _record_from_sums(sm[0], sm[1], sm[2], self.grid, spec)
+                    rec.step = int(st)
+                    rec.tau = int(st) * spec.dtau
+                    checks.append(rec)
+                if not fixed:
+                    code = nstatus()
+                    if code == 3:
+                        raise ZeroNormError("field collapsed to zero during evolution")
+                    if code == 4:
+                        raise DivergenceError("field norm diverged (check dtau against a^2/3)")
+            started = done
+            if tracker is not None and m > 0 and done == next_check and done < max_steps:
+                next_check += m
+                # the check on the state entering sweep done+1 (the per-step loop's
+                # fused measurement of that sweep)
+                sm = nmeasure()
+                rec = _record_from_sums(sm[0], sm[1], sm[2], self.grid, spec)
+                rec.step = done
+                rec.tau = done * spec.dtau
+                checks.append(rec)
+                verdict = tracker.update(rec.metric)
+                if verdict == DIVERGED:
+                    raise DivergenceError(
+                        f"energy rising at step {done} (E={rec.energy:.6g}); "
+                        f"dtau={spec.dtau} vs stability limit {stab.limit:.6g}")
+                if verdict == CONVERGED:
+                    converged_at = done
+                    started = done + 1
+                    break
+            if done % snap_freq == 0 and len(snaps) < max_snapshots:
+                snaps.append((done * spec.dtau, self.gather()))
+        converged = converged_at is not None
+        step_count = converged_at if converged else max_steps
+        final = self.gather() if gather else None
+        if dist_mode:
+            import torch
+
+            t = torch.tensor([float(self.halo_messages + comm.halo_messages() - h0)],
+                             dtype=torch.float64, device=s.torch_device())
+            self.group.dist.all_reduce(t)
+            self.halo_messages = int(t.item())
+        return final, checks, snaps, converged, step_count, started
 
     # -- parity across slabs ---------------------------------------------------
     def _impose(self, constraints, tag):
@@ -392,6 +510,12 @@ class SlabEngine:
         return Field3D(spec, values)
 
 
+def _axis_of(c) -> int:
+    from .states import _AXES
+
+    return _AXES[c.axis]
+
+
 def _make_slabs_local(grid, part, initial, seed):
     from .device import Slab
     from ._lib import device_count
@@ -437,7 +561,8 @@ def evolve_parallel(grid: PotentialGrid, *, workers: int, initial: Field3D | Non
                     snap_freq: int | None = None, constraints=(), max_steps: int = 1_000_000,
                     max_snapshots: int = 8, reimpose_freq: int | None = None,
                     timeout: float = 300.0, scatter_initial: bool = False,
-                    slab_factory=None) -> EvolutionState | None:
+                    slab_factory=None, native: bool = True, norm_every: int = 1,
+                    fixed: bool = False) -> EvolutionState | None:
     """Slab-decomposed convergence run (parallel.py:523-594); one slab per GPU.
 
     ``transport="inproc"`` drives all slabs from this process and returns
@@ -458,7 +583,7 @@ def evolve_parallel(grid: PotentialGrid, *, workers: int, initial: Field3D | Non
 
     if transport == "inproc":
         slabs = _make_slabs_local(grid, part, initial, seed)
-        engine = SlabEngine(grid, part, slabs, list(range(workers)), _LocalGroup(slabs))
+        engine = SlabEngine(grid, part, slabs, list(range(workers)), _LocalGroup(slabs, native))
     elif transport in ("nccl", "tcp", "dist"):
         import torch.distributed as dist
 
@@ -482,17 +607,25 @@ def evolve_parallel(grid: PotentialGrid, *, workers: int, initial: Field3D | Non
         else:
             init_planes = _initial_planes(spec, initial, seed, lo, hi)
         slab.set_field(init_planes, 0)
-        engine = SlabEngine(grid, part, [slab], [r], _DistGroup(slab, r, part))
+        comm = None
+        if slab_factory is None and native and dist.get_backend() == "nccl":
+            from .device import Comm
+
+            comm = Comm.from_process_group(slab.device)
+        engine = SlabEngine(grid, part, [slab], [r], _DistGroup(slab, r, part, comm))
     else:
         raise ConfigError(f"unknown transport {transport!r}")
 
     try:
         final, checks, snaps, converged, step_count, started = engine.run(
             tol=tol, check_freq=check_freq, snap_freq=snap_freq, reimpose_freq=reimpose_freq,
-            max_steps=max_steps, max_snapshots=max_snapshots, constraints=constraints)
+            max_steps=max_steps, max_snapshots=max_snapshots, constraints=constraints,
+            norm_every=norm_every, fixed=fixed)
     finally:
         for s in engine.slabs:
             s.close()
+        if isinstance(engine.group, _DistGroup) and engine.group.comm is not None:
+            engine.group.comm.close()
     if final is None:
         return None
     return EvolutionState(psi=final, tau=step_count * spec.dtau, step_count=step_count,

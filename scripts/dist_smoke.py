@@ -17,9 +17,9 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
-from paper_0904_0939_b200 import (LatticeSpec, SymmetryConstraint, allocate, evolve_parallel,
-                                  evolve_to_convergence, fill_random_gaussian, harmonic,
-                                  impose_inplace)
+from paper_0904_0939_b200 import (LatticeSpec, SymmetryConstraint, allocate, evolve_fixed,
+                                  evolve_parallel, evolve_to_convergence, fill_random_gaussian,
+                                  harmonic, impose_inplace)
 
 
 def main():
@@ -34,19 +34,44 @@ def main():
     cs = [SymmetryConstraint("x", "antisymmetric"), SymmetryConstraint("y", "symmetric")]
     for c in cs:
         impose_inplace(init.values, spec.N, c)
-    st = evolve_parallel(grid, workers=world, initial=init, transport="nccl", tol=1e-300,
-                         check_freq=20, max_steps=100, max_snapshots=0, constraints=cs)
+    ok = True
+    for native in (True, False):
+        st = evolve_parallel(grid, workers=world, initial=init, transport="nccl", tol=1e-300,
+                             check_freq=20, max_steps=100, max_snapshots=0, constraints=cs,
+                             native=native)
+        if rank == 0:
+            ref = evolve_to_convergence(init, grid, tol=1e-300, check_freq=20, max_steps=100,
+                                        max_snapshots=0, constraints=cs)
+            same = np.array_equal(st.psi.values, ref.psi.values)
+            e_same = [c.energy for c in st.checks] == [c.energy for c in ref.checks]
+            print(f"dist_smoke world={world} native={native}: psi bitwise {same}, energies "
+                  f"bitwise {e_same}, halo messages {st.halo_messages}, "
+                  f"sweeps {st.sweeps_started} vs {ref.sweeps_started}", flush=True)
+            ok = ok and same and e_same
+        else:
+            assert st is None
+    # converging run: stop at the same check, same state
+    st = evolve_parallel(grid, workers=world, initial=init, transport="nccl", tol=1e-5,
+                         check_freq=10, max_steps=4000, max_snapshots=0, constraints=cs)
     if rank == 0:
-        ref = evolve_to_convergence(init, grid, tol=1e-300, check_freq=20, max_steps=100,
+        ref = evolve_to_convergence(init, grid, tol=1e-5, check_freq=10, max_steps=4000,
                                     max_snapshots=0, constraints=cs)
+        same = (np.array_equal(st.psi.values, ref.psi.values) and st.step_count == ref.step_count
+                and st.converged == ref.converged)
+        print(f"dist_smoke converging: bitwise {same}, steps {st.step_count} vs "
+              f"{ref.step_count}, converged {st.converged}", flush=True)
+        ok = ok and same
+    # fixed-step recipe (fused observables, renormalisation every 20)
+    st = evolve_parallel(grid, workers=world, initial=init, transport="nccl", check_freq=20,
+                         max_steps=100, max_snapshots=0, norm_every=20, fixed=True)
+    if rank == 0:
+        ref = evolve_fixed(init, grid, 100, 20, norm_every=20)
         same = np.array_equal(st.psi.values, ref.psi.values)
         e_same = [c.energy for c in st.checks] == [c.energy for c in ref.checks]
-        print(f"dist_smoke world={world}: psi bitwise {same}, energies bitwise {e_same}, "
-              f"halo messages {st.halo_messages}", flush=True)
-        if not (same and e_same):
-            sys.exit(1)
-    else:
-        assert st is None
+        print(f"dist_smoke fixed: psi bitwise {same}, energies bitwise {e_same}", flush=True)
+        ok = ok and same and e_same
+    if rank == 0 and not ok:
+        sys.exit(1)
     dist.destroy_process_group()
 
 

@@ -229,3 +229,56 @@ def test_fused_norm_partials_equal_standalone(gpu_lib, n):
         s.reduce(1, n, F_NORM, combine=False)
         alone = s.read_sums()[0][3].copy()
     assert np.array_equal(fused, alone)
+
+
+@pytest.mark.parametrize("n,widths,steps,every,t2", [
+    (10, (2, 3, 5), 41, 10, True),
+    (40, (13, 14, 13), 61, 20, True),
+    (40, (20, 20), 60, 0, True),
+    (100, (34, 33, 33), 45, 20, True),
+    (100, (50, 50), 30, 10, False),
+])
+def test_multi_slab_run_matches_whole_lattice(gpu_lib, n, widths, steps, every, t2):
+    """psg_run_multi (slabs tiling the lattice, halos by peer copies, two-sweep
+    passes with two halo planes per face) gives the bits of the whole-lattice
+    run: field, check sums and the measured observables."""
+    from paper_0904_0939_b200.device import measure_multi, run_multi
+
+    spec = LatticeSpec(N=n, a=0.3, m=1.0, dtau=0.3 * 0.3 / 4.0)
+    rng = np.random.default_rng(n + 17)
+    ext = n + 2
+    psi0 = np.zeros((ext,) * 3)
+    psi0[1:-1, 1:-1, 1:-1] = rng.uniform(-0.5, 0.5, (n, n, n))
+    v = np.zeros((ext,) * 3)
+    v[1:-1, 1:-1, 1:-1] = rng.uniform(-1.0, 3.0, (n, n, n))
+    with Slab(spec) as whole:
+        whole.set_temporal(t2)
+        whole.set_field(psi0)
+        whole.set_potential(v)
+        idx_w, sums_w, _ = whole.run(steps, measure_every=every, norm_every=every or 1)
+        want = whole.get_field()
+        meas_w = measure_multi([whole])
+    slabs = []
+    try:
+        lo = 1
+        for w in widths:
+            s = Slab(spec, w=w, x_lo=lo)
+            s.set_temporal(t2)
+            s.set_field(psi0[lo - 1:lo + w + 1])
+            s.set_potential(v[lo - 1:lo + w + 1])
+            slabs.append(s)
+            lo += w
+        idx_m, sums_m, _ = run_multi(slabs, steps, measure_every=every, norm_every=every or 1)
+        got = np.zeros_like(want)
+        for s in slabs:
+            got[s.x_lo:s.x_lo + s.w] = s.get_field(1, s.w)
+        meas_m = measure_multi(slabs)
+        if t2 and steps > 4:
+            assert sum(s.launches() for s in slabs) > 0
+    finally:
+        for s in slabs:
+            s.close()
+    assert np.array_equal(got[1:-1], want[1:-1])
+    assert np.array_equal(idx_m, idx_w)
+    assert np.array_equal(sums_m, sums_w)
+    assert np.array_equal(meas_m, meas_w)
