@@ -83,6 +83,11 @@ int64_t psg_row_pitch(int64_t n);
  * returns the cached memory of `device` to the driver. */
 int psg_trim_memory(int device);
 
+/* Contiguous copies between device memory (on `device`) and host memory at
+ * link rate also for pageable host memory (pinned staging, host threads). */
+int psg_copy_to_host(int device, void* host, const void* dev, int64_t bytes);
+int psg_copy_to_device(int device, void* dev, const void* host, int64_t bytes);
+
 /* numpy.sum replica (pairwise, 8 accumulators, 128 blocks) on the device:
  * replaces observables.combine_plane_sums (observables.py:32-34) where the
  * combine must happen without a host round trip.  out[0] = sum(a[0..n)). */
@@ -160,7 +165,9 @@ double* psg_plane_ptr(psg_slab* s, int which, int64_t p);
 /* Upload `count` planes of a dense host field (ext x ext doubles each,
  * C order) into local planes first..first+count-1 of BOTH psi buffers and
  * reset the pending normalisation scale to 1.  Padding rows/cols are
- * copied as given (evolve.step carries padding over, evolve.py:45-53). */
+ * copied as given (evolve.step carries padding over, evolve.py:45-53).
+ * The dense planes (here and in psg_get_field / psg_set_potential) may also
+ * be device memory on the slab's device: then no host copy is made. */
 int psg_set_field(psg_slab* s, const double* host, int64_t first, int64_t count);
 
 /* Download local planes first..first+count-1 of the current state,

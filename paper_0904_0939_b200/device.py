@@ -140,12 +140,40 @@ class Slab:
         planes = self._planes_arg(planes)
         check(self._lib.psg_set_field(self._h, dptr(planes), first, planes.shape[0]))
 
-    def get_field(self, first: int = 0, count: int | None = None) -> np.ndarray:
-        """Download local planes (materialised state)."""
+    def get_field(self, first: int = 0, count: int | None = None,
+                  out: np.ndarray | None = None) -> np.ndarray:
+        """Download local planes (materialised state), into ``out`` if given
+        (C-contiguous float64 of shape (count, ext, ext))."""
         count = self.planes - first if count is None else count
-        out = np.empty((count, self.ext, self.ext))
+        if out is None:
+            out = np.empty((count, self.ext, self.ext))
+        elif (out.dtype != np.float64 or not out.flags.c_contiguous
+              or out.shape != (count, self.ext, self.ext)):
+            raise ConfigError("out must be C-contiguous float64 (count, ext, ext)")
         check(self._lib.psg_get_field(self._h, dptr(out), first, count))
         return out
+
+    def set_field_device(self, tensor, first: int = 0):
+        """Upload dense planes held in a CUDA tensor on this slab's device
+        (shape (count, ext, ext), float64, contiguous): re-pitched on the device."""
+        self._check_dense_tensor(tensor)
+        check(self._lib.psg_set_field(self._h, ctypes.cast(tensor.data_ptr(), _lib._dp), first,
+                                      tensor.shape[0]))
+
+    def get_field_device(self, tensor, first: int = 0):
+        """Download local planes into a CUDA tensor on this slab's device."""
+        self._check_dense_tensor(tensor)
+        check(self._lib.psg_get_field(self._h, ctypes.cast(tensor.data_ptr(), _lib._dp), first,
+                                      tensor.shape[0]))
+        return tensor
+
+    def _check_dense_tensor(self, t):
+        import torch
+
+        if (t.dtype != torch.float64 or not t.is_cuda or t.device.index != self.device
+                or not t.is_contiguous() or t.dim() != 3 or tuple(t.shape[1:]) != (self.ext, self.ext)):
+            raise ConfigError("expected a contiguous float64 CUDA tensor (count, ext, ext) on the "
+                              "slab's device")
 
     def set_potential(self, planes: np.ndarray, first: int = 0, owner=None):
         planes = self._planes_arg(planes)
@@ -330,6 +358,23 @@ class Slab:
     def status(self) -> int:
         """Sticky device status: 0 ok, 3 zero norm, 4 non-finite (read_sums scal[9])."""
         return int(self.read_sums()[1][9])
+
+
+def copy_to_host(device: int, host: np.ndarray, tensor):
+    """Contiguous CUDA tensor -> host array at link rate (staged for pageable memory)."""
+    if not host.flags.c_contiguous or host.nbytes != tensor.numel() * tensor.element_size():
+        raise ConfigError("host array must be contiguous and of the tensor's size")
+    check(_lib.load().psg_copy_to_host(device, host.ctypes.data, tensor.data_ptr(), host.nbytes))
+    return host
+
+
+def copy_to_device(device: int, tensor, host: np.ndarray):
+    """Host array -> contiguous CUDA tensor at link rate."""
+    host = np.ascontiguousarray(host)
+    if host.nbytes != tensor.numel() * tensor.element_size():
+        raise ConfigError("host array must be of the tensor's size")
+    check(_lib.load().psg_copy_to_device(device, tensor.data_ptr(), host.ctypes.data, host.nbytes))
+    return tensor
 
 
 def run_multi(slabs, steps: int, measure_every: int = 0, norm_every: int = 1,

@@ -491,23 +491,68 @@ class SlabEngine:
         if isinstance(self.group, _DistGroup):
             import torch
 
+            from .device import copy_to_host
+
             s = self.slabs[0]
             dist = self.group.dist
-            mine = torch.from_numpy(np.ascontiguousarray(s.get_field(1, s.w))).to(s.torch_device())
             rank = self.ranks[0]
+            if not s.torch_device().type == "cuda":   # CPU test slabs over gloo
+                mine = torch.from_numpy(np.ascontiguousarray(s.get_field(1, s.w)))
+                if rank == 0:
+                    parts = [mine] + [torch.empty_like(mine) for _ in range(self.part.M - 1)]
+                    for src in range(1, self.part.M):
+                        dist.recv(parts[src], src)
+                    values = np.zeros((ext, ext, ext))
+                    values[1:-1] = torch.cat(parts).numpy()
+                    return Field3D(spec, values)
+                dist.send(mine, 0)
+                return None
+            dev = s.torch_device()
             if rank == 0:
-                parts = [mine] + [torch.empty_like(mine) for _ in range(self.part.M - 1)]
-                for src in range(1, self.part.M):
-                    dist.recv(parts[src], src)
                 values = np.zeros((ext, ext, ext))
-                values[1:-1] = torch.cat(parts).cpu().numpy()
+                s.get_field(1, s.w, out=values[s.x_lo:s.x_lo + s.w])
+                buf = torch.empty((s.w, ext, ext), dtype=torch.float64, device=dev)
+                for src in range(1, self.part.M):
+                    lo, hi = self.part.x_range(src)
+                    dist.recv(buf, src)
+                    torch.cuda.current_stream(dev).synchronize()
+                    copy_to_host(s.device, values[lo:hi + 1], buf)
                 return Field3D(spec, values)
+            mine = torch.empty((s.w, ext, ext), dtype=torch.float64, device=dev)
+            s.get_field_device(mine, 1)
             dist.send(mine, 0)
+            torch.cuda.current_stream(dev).synchronize()
             return None
         values = np.zeros((ext, ext, ext))
         for s in self.slabs:
             values[s.x_lo:s.x_lo + s.w] = s.get_field(1, s.w)
         return Field3D(spec, values)
+
+
+_COMMS: dict = {}
+
+
+def get_comm(device: int):
+    """The native NCCL communicator over the default torch process group for
+    this device, created once per process group and reused (NCCL
+    initialisation costs far more than a run's setup)."""
+    import torch.distributed as dist
+
+    from .device import Comm
+
+    key = (id(dist.group.WORLD), dist.get_rank(), dist.get_world_size(), device)
+    c = _COMMS.get(key)
+    if c is None or c.handle is None:
+        c = Comm.from_process_group(device)
+        _COMMS[key] = c
+    return c
+
+
+def release_comms():
+    """Destroy the cached communicators (before destroying the process group)."""
+    for c in _COMMS.values():
+        c.close()
+    _COMMS.clear()
 
 
 def _axis_of(c) -> int:
@@ -603,15 +648,12 @@ def evolve_parallel(grid: PotentialGrid, *, workers: int, initial: Field3D | Non
             slab = slab_factory(spec, part.W, lo, r)
         slab.load_grid(grid)
         if scatter_initial:
-            init_planes = _scatter_initial(slab, part, r, initial, spec)
+            _scatter_initial(slab, part, r, initial, spec)
         else:
-            init_planes = _initial_planes(spec, initial, seed, lo, hi)
-        slab.set_field(init_planes, 0)
+            slab.set_field(_initial_planes(spec, initial, seed, lo, hi), 0)
         comm = None
         if slab_factory is None and native and dist.get_backend() == "nccl":
-            from .device import Comm
-
-            comm = Comm.from_process_group(slab.device)
+            comm = get_comm(slab.device)
         engine = SlabEngine(grid, part, [slab], [r], _DistGroup(slab, r, part, comm))
     else:
         raise ConfigError(f"unknown transport {transport!r}")
@@ -624,8 +666,6 @@ def evolve_parallel(grid: PotentialGrid, *, workers: int, initial: Field3D | Non
     finally:
         for s in engine.slabs:
             s.close()
-        if isinstance(engine.group, _DistGroup) and engine.group.comm is not None:
-            engine.group.comm.close()
     if final is None:
         return None
     return EvolutionState(psi=final, tau=step_count * spec.dtau, step_count=step_count,
@@ -635,21 +675,41 @@ def evolve_parallel(grid: PotentialGrid, *, workers: int, initial: Field3D | Non
 
 
 def _scatter_initial(slab, part, rank, initial, spec):
+    """Rank 0 holds the start field; every slab receives its planes (device
+    buffers over NCCL, re-pitched on the device: no host round trip on the
+    receivers).  Sets the slab's field; returns None."""
     import torch
     import torch.distributed as dist
 
+    from .device import copy_to_device
+
     ext = spec.extent
     w = part.W
-    buf = torch.zeros((w + 2, ext, ext), dtype=torch.float64, device=slab.torch_device())
+    dev = slab.torch_device()
+
+    def shell(t):
+        # the worker's start planes: halo planes zero, Dirichlet j / k borders
+        t[0].zero_()
+        t[-1].zero_()
+        t[:, 0, :] = 0.0
+        t[:, -1, :] = 0.0
+        t[:, :, 0] = 0.0
+        t[:, :, -1] = 0.0
+        return t
+
+    buf = torch.empty((w + 2, ext, ext), dtype=torch.float64, device=dev)
     if rank == 0:
         for dst in range(part.M):
             lo, hi = part.x_range(dst)
-            planes = np.zeros((w + 2, ext, ext))
-            planes[1:w + 1] = initial.values[lo:hi + 1]
+            copy_to_device(slab.device, buf, initial.values[lo - 1:hi + 2])
+            shell(buf)
             if dst == 0:
-                buf.copy_(torch.from_numpy(planes))
+                slab.set_field_device(buf, 0)
             else:
-                dist.send(torch.from_numpy(planes).to(buf.device), dst)
+                dist.send(buf, dst)
+                torch.cuda.current_stream(dev).synchronize()
     else:
         dist.recv(buf, 0)
-    return buf.cpu().numpy()
+        torch.cuda.current_stream(dev).synchronize()
+        slab.set_field_device(buf, 0)
+    return None

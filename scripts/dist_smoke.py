@@ -70,6 +70,18 @@ def main():
         e_same = [c.energy for c in st.checks] == [c.energy for c in ref.checks]
         print(f"dist_smoke fixed: psi bitwise {same}, energies bitwise {e_same}", flush=True)
         ok = ok and same and e_same
+    # scatter from rank 0 / gather to rank 0 through device buffers
+    st = evolve_parallel(grid, workers=world, initial=init if rank == 0 else None,
+                         transport="nccl", scatter_initial=True, check_freq=20, max_steps=60,
+                         max_snapshots=0, norm_every=20, fixed=True)
+    if rank == 0:
+        ref = evolve_fixed(init, grid, 60, 20, norm_every=20)
+        same = np.array_equal(st.psi.values, ref.psi.values)
+        print(f"dist_smoke scatter/gather: psi bitwise {same}", flush=True)
+        ok = ok and same
+    from paper_0904_0939_b200.parallel import release_comms
+
+    release_comms()
     if rank == 0 and not ok:
         sys.exit(1)
     dist.destroy_process_group()
