@@ -366,10 +366,12 @@ def run_single(args):
 
 
 def weak_n(n1: int, m: int) -> int:
-    """Lattice size with ~n1^3 sites per GPU on m GPUs, a multiple of m."""
+    """Lattice size with ~n1^3 sites per GPU on m GPUs: the multiple of
+    lcm(64, m) nearest n1 * m^(1/3) (64-column tiles stay full; m equal slabs)."""
     if m == 1:
         return n1
-    return max(m, int(round(n1 * m ** (1.0 / 3.0) / m)) * m)
+    step = 64 * m // math.gcd(64, m)
+    return max(step, int(round(n1 * m ** (1.0 / 3.0) / step)) * step)
 
 
 def run_dist(args):
@@ -464,8 +466,8 @@ def run_dist(args):
             "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": w.name, "N": n, "measure_every": m, "norm_every": m,
-                       "weak": f"{base.name} recipe (box side {base.N * base.a:g}) on N = "
-                               f"round({base.N}*M^(1/3)) (multiple of M): "
+                       "weak": f"{base.name} recipe (box side {base.N * base.a:g}) on N = the "
+                               f"multiple of lcm(64, M) nearest {base.N}*M^(1/3): "
                                f"{n ** 3 / world / 1e6:.2f} M sites per GPU",
                        "parallelism": f"z-slabs x{world} (NCCL: two halo planes per face every "
                                       f"other sweep, overlapped; exact all-reduce of plane sums)",
