@@ -104,6 +104,10 @@ class Slab:
         """TMA pipeline depth of the 16-row two-sweep pass: 6 or 9."""
         self.set_option(5, stages)
 
+    def set_t2_alt(self, on: int):
+        """Two-sweep passes alternate their chunk order (default 1)."""
+        self.set_option(6, on)
+
     def set_coef_check(self, on: int):
         """Always take the range-checked coefficient path (default: only when needed)."""
         self.set_option(4, on)
