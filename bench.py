@@ -440,7 +440,10 @@ def run_dist(args):
 
     # ---- e2e: the public multi-GPU API from host arrays (rank 0 holds psi0) ----
     ext = n + 2
-    vfull = workloads.potential_planes(w, spec, 0, ext)
+    # the grid's V array is lattice-sized, but a rank only reads its own planes
+    # (load_grid): fill those (untouched zero pages cost no host memory)
+    vfull = np.zeros((ext, ext, ext))
+    vfull[lo - 1:lo + part.W + 1] = workloads.potential_planes(w, spec, lo - 1, part.W + 2)
     pgrid = PotentialGrid(spec=spec, v=vfull, v_inf=0.0, unbounded=False, name="custom")
     init = None
     if rank == 0:
