@@ -561,10 +561,10 @@ def _axis_of(c) -> int:
     return _AXES[c.axis]
 
 
-def _make_slabs_local(grid, part, initial, seed):
+def _make_slabs_local(grid, part, initial, seed, initial_file=None):
     from .device import Slab
     from ._lib import device_count
-    from .lattice import uniform_plane, gaussian_plane
+    from .multires import load_slab_planes
 
     spec = grid.spec
     ndev = max(1, device_count())
@@ -573,7 +573,10 @@ def _make_slabs_local(grid, part, initial, seed):
         lo, hi = part.x_range(r)
         s = Slab(spec, w=part.W, x_lo=lo, device=r % ndev)
         s.load_grid(grid)
-        s.set_field(_initial_planes(spec, initial, seed, lo, hi), 0)
+        if initial_file is not None:
+            load_slab_planes(s, initial_file)
+        else:
+            s.set_field(_initial_planes(spec, initial, seed, lo, hi), 0)
         slabs.append(s)
     return slabs
 
@@ -607,7 +610,8 @@ def evolve_parallel(grid: PotentialGrid, *, workers: int, initial: Field3D | Non
                     max_snapshots: int = 8, reimpose_freq: int | None = None,
                     timeout: float = 300.0, scatter_initial: bool = False,
                     slab_factory=None, native: bool = True, norm_every: int = 1,
-                    fixed: bool = False) -> EvolutionState | None:
+                    fixed: bool = False, initial_file=None, checkpoint_path=None,
+                    gather: bool = True) -> EvolutionState | None:
     """Slab-decomposed convergence run (parallel.py:523-594); one slab per GPU.
 
     ``transport="inproc"`` drives all slabs from this process and returns
@@ -620,14 +624,14 @@ def evolve_parallel(grid: PotentialGrid, *, workers: int, initial: Field3D | Non
     part = partition(spec, workers)
     if check_freq < 1:
         raise ConfigError("check_freq must be >= 1")
-    if initial is None and seed is None and not scatter_initial:
-        raise ConfigError("evolve_parallel needs an initial field or a seed")
+    if initial is None and seed is None and not scatter_initial and initial_file is None:
+        raise ConfigError("evolve_parallel needs an initial field, a seed or an initial_file")
     snap_freq = snap_freq if snap_freq else 10 * check_freq
     reimpose_freq = reimpose_freq if reimpose_freq else check_freq
     constraints = tuple(constraints)
 
     if transport == "inproc":
-        slabs = _make_slabs_local(grid, part, initial, seed)
+        slabs = _make_slabs_local(grid, part, initial, seed, initial_file)
         engine = SlabEngine(grid, part, slabs, list(range(workers)), _LocalGroup(slabs, native))
     elif transport in ("nccl", "tcp", "dist"):
         import torch.distributed as dist
@@ -647,7 +651,11 @@ def evolve_parallel(grid: PotentialGrid, *, workers: int, initial: Field3D | Non
         else:
             slab = slab_factory(spec, part.W, lo, r)
         slab.load_grid(grid)
-        if scatter_initial:
+        if initial_file is not None:
+            from .multires import load_slab_planes
+
+            load_slab_planes(slab, initial_file)
+        elif scatter_initial:
             _scatter_initial(slab, part, r, initial, spec)
         else:
             slab.set_field(_initial_planes(spec, initial, seed, lo, hi), 0)
@@ -662,11 +670,20 @@ def evolve_parallel(grid: PotentialGrid, *, workers: int, initial: Field3D | Non
         final, checks, snaps, converged, step_count, started = engine.run(
             tol=tol, check_freq=check_freq, snap_freq=snap_freq, reimpose_freq=reimpose_freq,
             max_steps=max_steps, max_snapshots=max_snapshots, constraints=constraints,
-            norm_every=norm_every, fixed=fixed)
+            norm_every=norm_every, fixed=fixed, gather=gather)
+        if checkpoint_path is not None:
+            from .multires import save_wavefunction_slabs
+
+            if isinstance(engine.group, _DistGroup):
+                save_wavefunction_slabs(engine.slabs, checkpoint_path, step_count,
+                                        rank=engine.ranks[0], barrier=engine.group.dist.barrier)
+            else:
+                save_wavefunction_slabs(engine.slabs, checkpoint_path, step_count)
     finally:
         for s in engine.slabs:
             s.close()
-    if final is None:
+    if final is None and (gather or not (isinstance(engine.group, _LocalGroup)
+                                         or engine.ranks[0] == 0)):
         return None
     return EvolutionState(psi=final, tau=step_count * spec.dtau, step_count=step_count,
                           snapshots=[(t, f) for t, f in snaps if f is not None], checks=checks,

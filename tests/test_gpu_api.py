@@ -508,3 +508,45 @@ def test_nccl_slab_path_single_rank(gpu_lib):
                        cwd=root, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
     assert "psi bitwise True" in r.stdout and "energies bitwise True" in r.stdout
+
+
+# ---------------------------------------------------------------- checkpoints
+class TestSlabCheckpoint:
+    def test_streamed_checkpoint_is_the_assembled_file(self, gpu_lib, tmp_path):
+        """Every slab writes its own planes into one QWF1 file: byte-identical to
+        save_wavefunction of the gathered field; resuming from it per slab gives
+        the bits of resuming from the loaded field."""
+        from paper_0904_0939_b200.multires import load_wavefunction, save_wavefunction
+
+        spec = LatticeSpec(N=20, a=0.5, m=1.0, dtau=0.0625)
+        grid = harmonic(spec)
+        init = fill_random_gaussian(allocate(spec), 3)
+        a, b = tmp_path / "slabs.qwf", tmp_path / "whole.qwf"
+        st = evolve_parallel(grid, workers=4, initial=init, tol=1e-300, check_freq=10,
+                             max_steps=30, max_snapshots=0, checkpoint_path=a)
+        save_wavefunction(st.psi, b, step_count=st.step_count)
+        assert a.read_bytes() == b.read_bytes()
+        resumed = evolve_parallel(grid, workers=2, initial_file=a, tol=1e-300, check_freq=10,
+                                  max_steps=20, max_snapshots=0)
+        field, _ = load_wavefunction(a)
+        ref = evolve_parallel(grid, workers=2, initial=field, tol=1e-300, check_freq=10,
+                              max_steps=20, max_snapshots=0)
+        assert np.array_equal(resumed.psi.values, ref.psi.values)
+
+    def test_load_slab_planes_validates(self, gpu_lib, tmp_path):
+        from paper_0904_0939_b200.device import Slab
+        from paper_0904_0939_b200.errors import FormatError
+        from paper_0904_0939_b200.multires import load_slab_planes, save_wavefunction
+
+        spec = LatticeSpec(N=8, a=0.5, m=1.0, dtau=0.0625)
+        f = fill_random_gaussian(allocate(spec), 5)
+        p = tmp_path / "f.qwf"
+        save_wavefunction(f, p)
+        other = LatticeSpec(N=10, a=0.5, m=1.0, dtau=0.0625)
+        with Slab(other, w=5, x_lo=1) as s:
+            with pytest.raises(FormatError):
+                load_slab_planes(s, p)
+        with Slab(spec, w=4, x_lo=5) as s:
+            load_slab_planes(s, p)
+            got = s.get_field()
+        assert np.array_equal(got[:-1], f.values[4:9]) and not got[-1].any()
