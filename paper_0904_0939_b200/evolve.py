@@ -314,51 +314,60 @@ def evolve_to_convergence(initial: Field3D, grid: PotentialGrid, tol: float = 1e
     if reimpose_freq is None:
         reimpose_freq = check_freq
     constraints = tuple(constraints)
-    pairs = _constraint_pairs(constraints)
-    tracker = ConvergenceTracker(tol)
-
     start_values = _dirichlet_start(initial)
     slab = Slab(spec)
-    snapshots: list = []
-    checks: list = []
     try:
         slab.set_field(start_values)
         slab.load_grid(grid)
-
-        def finish(step_count: int, converged: bool) -> EvolutionState:
-            return EvolutionState(psi=Field3D(spec, slab.get_field()),
-                                  tau=step_count * spec.dtau, step_count=step_count,
-                                  snapshots=snapshots, checks=checks, converged=converged,
-                                  constraints=constraints, sweeps_started=step_count)
-
-        s = 0
-        while s < max_steps:
-            if s > 0 and s % check_freq == 0:
-                num, den, r2 = measure_device(slab)
-                rec = _record_from_sums(num, den, r2, grid, spec)
-                rec.step = s
-                rec.tau = s * spec.dtau
-                checks.append(rec)
-                verdict = tracker.update(rec.metric)
-                if verdict == DIVERGED:
-                    raise DivergenceError(
-                        f"energy rising at step {s} (E={rec.energy:.6g}); "
-                        f"dtau={spec.dtau} vs stability limit {stab.limit:.6g}")
-                if verdict == CONVERGED:
-                    return finish(s, True)
-            nxt = min(max_steps, (s // check_freq + 1) * check_freq)
-            if len(snapshots) < max_snapshots:
-                nxt = min(nxt, (s // snap_freq + 1) * snap_freq)
-            slab.run(nxt - s, measure_every=0, norm_every=1,
-                     reimpose_every=reimpose_freq if pairs else 0, constraints=pairs,
-                     step_offset=s)
-            _raise_status(slab.status(), f"before step {nxt}")
-            s = nxt
-            if s % snap_freq == 0 and len(snapshots) < max_snapshots:
-                snapshots.append((s * spec.dtau, Field3D(spec, slab.get_field())))
-        return finish(max_steps, False)
+        step_count, converged, checks, snapshots = converge_on_slab(
+            slab, grid, tol=tol, check_freq=check_freq, snap_freq=snap_freq,
+            constraints=constraints, max_steps=max_steps, max_snapshots=max_snapshots,
+            reimpose_freq=reimpose_freq)
+        return EvolutionState(psi=Field3D(spec, slab.get_field()), tau=step_count * spec.dtau,
+                              step_count=step_count, snapshots=snapshots, checks=checks,
+                              converged=converged, constraints=constraints,
+                              sweeps_started=step_count)
     finally:
         slab.close()
+
+
+def converge_on_slab(slab, grid: PotentialGrid, *, tol: float, check_freq: int, snap_freq: int,
+                     constraints=(), max_steps: int, max_snapshots: int, reimpose_freq: int):
+    """The evolve_to_convergence loop on a device-resident whole-lattice slab
+    (its field and potential already in place); leaves the final state on the
+    slab.  Returns (step_count, converged, checks, snapshots)."""
+    spec = slab.spec
+    stab = check_stability(spec)
+    pairs = _constraint_pairs(tuple(constraints))
+    tracker = ConvergenceTracker(tol)
+    snapshots: list = []
+    checks: list = []
+    s = 0
+    while s < max_steps:
+        if s > 0 and s % check_freq == 0:
+            num, den, r2 = measure_device(slab)
+            rec = _record_from_sums(num, den, r2, grid, spec)
+            rec.step = s
+            rec.tau = s * spec.dtau
+            checks.append(rec)
+            verdict = tracker.update(rec.metric)
+            if verdict == DIVERGED:
+                raise DivergenceError(
+                    f"energy rising at step {s} (E={rec.energy:.6g}); "
+                    f"dtau={spec.dtau} vs stability limit {stab.limit:.6g}")
+            if verdict == CONVERGED:
+                return s, True, checks, snapshots
+        nxt = min(max_steps, (s // check_freq + 1) * check_freq)
+        if len(snapshots) < max_snapshots:
+            nxt = min(nxt, (s // snap_freq + 1) * snap_freq)
+        slab.run(nxt - s, measure_every=0, norm_every=1,
+                 reimpose_every=reimpose_freq if pairs else 0, constraints=pairs,
+                 step_offset=s)
+        _raise_status(slab.status(), f"before step {nxt}")
+        s = nxt
+        if s % snap_freq == 0 and len(snapshots) < max_snapshots:
+            snapshots.append((s * spec.dtau, Field3D(spec, slab.get_field())))
+    return max_steps, False, checks, snapshots
 
 
 def evolve_fixed(initial: Field3D, grid: PotentialGrid, steps: int, measure_every: int,

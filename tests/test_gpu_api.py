@@ -550,3 +550,24 @@ class TestSlabCheckpoint:
             load_slab_planes(s, p)
             got = s.get_field()
         assert np.array_equal(got[:-1], f.values[4:9]) and not got[-1].any()
+
+
+def test_bootstrap_resident_matches_host_path(gpu_lib, monkeypatch):
+    """bootstrap_run with the stages resident on the GPU (resample slab to slab,
+    renormalise, carry coefficient, constraints, convergence loop) gives the
+    bits of the host-composed ladder."""
+    from paper_0904_0939_b200 import multires
+
+    def make_grid(spec):
+        return harmonic(spec)
+
+    ladder = [LatticeSpec(N=n, a=6.0 / n, m=1.0, dtau=(6.0 / n) ** 2 / 4.0) for n in (8, 12, 16)]
+    cs = [SymmetryConstraint("y", "antisymmetric")]
+    kw = dict(seed=4, tol=1e-7, check_freq=20, max_steps=4000, max_snapshots=0, constraints=cs,
+              carry_coefficients=[0.5])
+    resident = multires.bootstrap_run(ladder, make_grid, **kw)
+    monkeypatch.setattr(multires, "_RESIDENT", False)
+    host = multires.bootstrap_run(ladder, make_grid, **kw)
+    assert np.array_equal(resident.psi.values, host.psi.values)
+    assert [r.iterations for r in resident.stage_reports] == [r.iterations for r in host.stage_reports]
+    assert [c.energy for c in resident.checks] == [c.energy for c in host.checks]
