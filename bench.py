@@ -398,10 +398,9 @@ def run_dist(args):
     part = partition(spec, world)
     lo, hi = part.x_range(rank)
     slab = Slab(spec, w=part.W, x_lo=lo, device=local)
-    planes = np.zeros((part.W + 2, n + 2, n + 2))
-    planes[1:-1] = workloads.uniform_start(spec, first=lo, count=part.W)
-    slab.set_field(planes)
-    slab.set_potential(workloads.potential_planes(w, spec, lo - 1, part.W + 2))
+    # start field and potential generated on the device (bitwise the host
+    # recipes: Philox plane stream, Coulomb floor)
+    workloads.fill_slab(slab, w)
 
     class _G:  # the grid object the engine needs (v only used on the host for checks)
         pass

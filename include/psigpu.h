@@ -175,6 +175,23 @@ int psg_set_field(psg_slab* s, const double* host, int64_t first, int64_t count)
  * evolve.py:180). */
 int psg_get_field(psg_slab* s, double* host, int64_t first, int64_t count);
 
+/* Device-side inputs (no host copy of the field; 2048^3 runs):
+ * psg_fill_uniform: the seeded U(-0.5, 0.5) start of every interior site of
+ * the slab's planes, bitwise lattice.uniform_plane (numpy Philox4x64 keyed by
+ * seed, plane i at counter block (i-1)*ceil(N^2/4)); padding zero; pending
+ * normalisation reset.
+ * psg_fill_potential: V on the slab's planes, kind 0 harmonic (0.5 r) r,
+ * 1 Coulomb -1/max(r, a/2), 2 Cornell -alpha/max(r,a/2) + sigma max(r,a/2)
+ * (params alpha, sigma), 3 harmonic plus 8 Gaussian wells (params: centres
+ * [8][3] by storage axis, depths[8], widths[8]); r from the lattice centre as
+ * in workloads.py (bitwise, except the wells' exp: <= 1 ulp per term), then
+ * the same checks as psg_set_potential. */
+int psg_fill_uniform(psg_slab* s, uint64_t seed);
+/* Download potential planes (dense, like psg_get_field). */
+int psg_get_potential(psg_slab* s, double* host, int64_t first, int64_t count);
+int psg_fill_potential(psg_slab* s, int kind, const double* params, int nparams,
+                       int64_t* bad_site);
+
 /* Upload the potential for local planes first..first+count-1 (dense host
  * planes, ext x ext).  Returns PSG_ERR_SINGULAR and the offending global
  * site in bad_site[3] when 1 + (dtau/2) V == 0 (potential.py:103-110). */

@@ -56,6 +56,9 @@ SIGNATURES = {
     "psg_device_count": (c_int, []),
     "psg_row_pitch": (c_int64, [c_int64]),
     "psg_trim_memory": (c_int, [c_int]),
+    "psg_fill_uniform": (c_int, [c_void_p, ctypes.c_uint64]),
+    "psg_get_potential": (c_int, [c_void_p, _dp, c_int64, c_int64]),
+    "psg_fill_potential": (c_int, [c_void_p, c_int, _dp, c_int, _lp]),
     "psg_copy_to_host": (c_int, [c_int, c_void_p, c_void_p, c_int64]),
     "psg_copy_to_device": (c_int, [c_int, c_void_p, c_void_p, c_int64]),
     "psg_pairwise_sum_device": (c_int, [_dp, c_int64, _dp]),

@@ -190,6 +190,32 @@ class Slab:
         check(rc)
         self._v_owner = owner
 
+    def get_potential(self, first: int = 0, count: int | None = None) -> np.ndarray:
+        """Download potential planes (dense (count, ext, ext))."""
+        count = self.planes - first if count is None else count
+        out = np.empty((count, self.ext, self.ext))
+        check(self._lib.psg_get_potential(self._h, dptr(out), first, count))
+        return out
+
+    def fill_uniform(self, seed: int):
+        """The seeded U(-0.5, 0.5) start generated on the device (bitwise
+        lattice.uniform_plane for every interior plane of the slab)."""
+        check(self._lib.psg_fill_uniform(self._h, int(seed) & ((1 << 64) - 1)))
+
+    def fill_potential(self, kind: int, params=()):
+        """V generated on the device: kind 0 harmonic, 1 Coulomb (floored),
+        2 Cornell (alpha, sigma), 3 harmonic + 8 wells (centres, depths, widths)."""
+        prm = np.ascontiguousarray(np.asarray(params, dtype=np.float64).ravel())
+        bad = np.zeros(3, dtype=np.int64)
+        rc = self._lib.psg_fill_potential(self._h, int(kind), dptr(prm) if prm.size else None,
+                                          int(prm.size), lptr(bad))
+        if rc == 5:
+            i, j, k = (int(x) for x in bad)
+            raise SingularCoefficientError(
+                f"1 + (dtau/2) V = 0 at site ({i},{j},{k}); the potential must be regulated")
+        check(rc)
+        self._v_owner = None
+
     def set_coefficients(self, a_planes: np.ndarray, c_planes: np.ndarray, first: int = 0):
         a_planes = self._planes_arg(a_planes)
         c_planes = self._planes_arg(c_planes)

@@ -146,6 +146,28 @@ def potential_planes(w: Workload, spec: LatticeSpec, first: int, count: int) -> 
     return out
 
 
-__all__ = ["Workload", "CONFIGS", "scaled", "uniform_start", "uniform_field", "wells_params",
+POT_KINDS = {"harmonic": 0, "coulomb_floor": 1, "cornell": 2, "wells": 3}
+
+
+def device_potential(w: Workload):
+    """(kind, params) of the recipe's potential for Slab.fill_potential."""
+    kind = POT_KINDS[w.potential]
+    if w.potential == "cornell":
+        return kind, (0.5, 1.0)
+    if w.potential == "wells":
+        centres, depths, widths = wells_params()
+        return kind, np.concatenate([centres.ravel(), depths, widths])
+    return kind, ()
+
+
+def fill_slab(slab, w: Workload, seed: int = PSI_SEED) -> None:
+    """Start field and potential of the recipe generated on the slab's device
+    (no host arrays: what makes 2048^3 practical)."""
+    slab.fill_uniform(seed)
+    kind, params = device_potential(w)
+    slab.fill_potential(kind, params)
+
+
+__all__ = ["Workload", "CONFIGS", "scaled", "device_potential", "fill_slab", "POT_KINDS", "uniform_start", "uniform_field", "wells_params",
            "potential_interior", "make_grid", "potential_planes", "PSI_SEED", "WELLS_SEED",
            "_radii"]

@@ -282,3 +282,33 @@ def test_multi_slab_run_matches_whole_lattice(gpu_lib, n, widths, steps, every, 
     assert np.array_equal(idx_m, idx_w)
     assert np.array_equal(sums_m, sums_w)
     assert np.array_equal(meas_m, meas_w)
+
+
+@pytest.mark.parametrize("n,w,x_lo", [(7, None, 1), (16, None, 1), (33, 11, 12), (64, 20, 45)])
+def test_device_inputs_match_host_recipes(gpu_lib, n, w, x_lo):
+    """fill_uniform is bitwise the host Philox plane stream; the harmonic,
+    Coulomb and Cornell potentials are bitwise the host expressions; the wells
+    differ by at most a few ulps (device exp)."""
+    from paper_0904_0939_b200 import workloads
+
+    spec = LatticeSpec(N=n, a=20.0 / n, m=1.0, dtau=(20.0 / n) ** 2 / 4.0)
+    ww = n if w is None else w
+    with Slab(spec, w=ww, x_lo=x_lo) as s:
+        s.fill_uniform(1234)
+        got = s.get_field()
+        want = np.zeros_like(got)
+        lo = max(x_lo - 1, 1)
+        hi = min(x_lo + ww, n)
+        want[lo - (x_lo - 1):hi - (x_lo - 1) + 1] = workloads.uniform_start(spec, 1234, lo,
+                                                                             hi - lo + 1)
+        assert np.array_equal(got, want)
+        for name in ("harmonic", "coulomb_floor", "cornell", "wells"):
+            rec = workloads.Workload("t", n, spec.a, 1, 1, name, None)
+            kind, params = workloads.device_potential(rec)
+            s.fill_potential(kind, params)
+            host = workloads.potential_planes(rec, spec, x_lo - 1, ww + 2)
+            dev = s.get_potential()
+            if name == "wells":
+                np.testing.assert_allclose(dev, host, rtol=1e-14, atol=1e-14)
+            else:
+                assert np.array_equal(dev, host), name
