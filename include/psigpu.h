@@ -86,6 +86,10 @@ int psg_trim_memory(int device);
 /* Contiguous copies between device memory (on `device`) and host memory at
  * link rate also for pageable host memory (pinned staging, host threads). */
 int psg_copy_to_host(int device, void* host, const void* dev, int64_t bytes);
+/* Page-locked host buffers, cached by size after release (downloads into them
+ * run at link rate); NULL on failure. */
+void* psg_host_alloc(int64_t bytes);
+void psg_host_free(void* p, int64_t bytes);
 int psg_copy_to_device(int device, void* dev, const void* host, int64_t bytes);
 
 /* numpy.sum replica (pairwise, 8 accumulators, 128 blocks) on the device:

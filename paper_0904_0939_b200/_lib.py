@@ -60,6 +60,8 @@ SIGNATURES = {
     "psg_get_potential": (c_int, [c_void_p, _dp, c_int64, c_int64]),
     "psg_fill_potential": (c_int, [c_void_p, c_int, _dp, c_int, _lp]),
     "psg_copy_to_host": (c_int, [c_int, c_void_p, c_void_p, c_int64]),
+    "psg_host_alloc": (c_void_p, [c_int64]),
+    "psg_host_free": (None, [c_void_p, c_int64]),
     "psg_copy_to_device": (c_int, [c_int, c_void_p, c_void_p, c_int64]),
     "psg_pairwise_sum_device": (c_int, [_dp, c_int64, _dp]),
     "psg_selftest_division": (c_int, [c_int64, ctypes.c_uint64, c_double, c_double,

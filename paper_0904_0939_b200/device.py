@@ -30,6 +30,37 @@ class _DeviceArray:
                                          "strides": None, "stream": None}
 
 
+class _PinnedBlock:
+    """Owner of a cached page-locked host buffer (psg_host_alloc); numpy
+    arrays viewing it keep it alive, and it returns to the cache on release."""
+
+    def __init__(self, nbytes: int):
+        self._lib = _lib.load()
+        self.nbytes = nbytes
+        self.ptr = self._lib.psg_host_alloc(nbytes)
+        if not self.ptr:
+            raise MemoryError("page-locked host allocation failed")
+        self.__array_interface__ = {"shape": (nbytes,), "typestr": "|u1",
+                                    "data": (self.ptr, False), "version": 3}
+
+    def __del__(self):
+        try:
+            if self.ptr:
+                self._lib.psg_host_free(self.ptr, self.nbytes)
+                self.ptr = None
+        except Exception:
+            pass
+
+
+PINNED_MIN_BYTES = 16 << 20
+
+
+def pinned_empty(shape) -> np.ndarray:
+    """float64 array in a cached page-locked buffer."""
+    n = int(np.prod(shape)) * 8
+    return np.asarray(_PinnedBlock(n)).view(np.float64).reshape(shape)
+
+
 class Slab:
     """One GPU's slab of local planes 0..w+1 (global x_lo-1 .. x_lo+w)."""
 
@@ -150,7 +181,9 @@ class Slab:
         (C-contiguous float64 of shape (count, ext, ext))."""
         count = self.planes - first if count is None else count
         if out is None:
-            out = np.empty((count, self.ext, self.ext))
+            shape = (count, self.ext, self.ext)
+            out = (pinned_empty(shape) if count * self.ext * self.ext * 8 >= PINNED_MIN_BYTES
+                   else np.empty(shape))
         elif (out.dtype != np.float64 or not out.flags.c_contiguous
               or out.shape != (count, self.ext, self.ext)):
             raise ConfigError("out must be C-contiguous float64 (count, ext, ext)")
