@@ -38,15 +38,17 @@ import torch
 from scripts.quick_bench import make
 torch.cuda.init()
 res = {}
+opts = dict(OPTS)
+ne = opts.pop("norm_every", 0)   # pseudo-option: renormalise every ne sweeps
 for n in NS:
     s = make(n)
-    for k, v in OPTS.items():
+    for k, v in opts.items():
         getattr(s, k)(v)
     st = torch.cuda.ExternalStream(s.stream)
     steps = STEPS[n]
-    s.run(20, 0, 0); s.sync()
+    s.run(20, 0, ne); s.sync()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(st); s.run(steps, 0, 0); e1.record(st); e1.synchronize()
+    e0.record(st); s.run(steps, 0, ne); e1.record(st); e1.synchronize()
     res[n] = e0.elapsed_time(e1) * 1e3 / steps
     s.close()
 print(json.dumps(res))
