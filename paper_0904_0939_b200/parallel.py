@@ -241,7 +241,7 @@ class SlabEngine:
         dist_mode = isinstance(self.group, _DistGroup)
         native_ok = (self.group.comm is not None if dist_mode else
                      getattr(self.group, "native", False))
-        if native_ok and not any(_axis_of(c) == 0 for c in constraints):
+        if native_ok:
             return self._run_native(tol=tol, check_freq=check_freq, snap_freq=snap_freq,
                                     reimpose_freq=reimpose_freq, max_steps=max_steps,
                                     max_snapshots=max_snapshots, constraints=constraints,
@@ -362,7 +362,11 @@ class SlabEngine:
         stab = check_stability(spec)
         tracker = None if fixed else ConvergenceTracker(tol)
         m = check_freq if measure_every is None else measure_every
-        pairs = [(_AXES[c.axis], int(c.sign)) for c in constraints]
+        # constraints along the slab axis need the mirror exchange: applied here
+        # between native segments (parity operations commute exactly, so the
+        # others can run inside the loop)
+        ax0 = tuple(c for c in constraints if _AXES[c.axis] == 0)
+        pairs = [(_AXES[c.axis], int(c.sign)) for c in constraints if _AXES[c.axis] != 0]
         checks, snaps = [], []
         converged_at = None
         h0 = comm.halo_messages() if dist_mode else 0
@@ -378,6 +382,8 @@ class SlabEngine:
                 nxt = min(nxt, (done // snap_freq + 1) * snap_freq)
             if tracker is not None and m > 0:
                 nxt = min(nxt, next_check)
+            if ax0:
+                nxt = min(nxt, (done // reimpose_freq + 1) * reimpose_freq)
             if nxt > done:
                 idx, sums, _ = nrun(nxt - done, measure_every=fused_m, norm_every=norm_every,
                                     reimpose_every=reimpose_freq if pairs else 0,
@@ -396,6 +402,8 @@ class SlabEngine:
                         raise ZeroNormError("field collapsed to zero during evolution")
                     if code == 4:
                         raise DivergenceError("field norm diverged (check dtau against a^2/3)")
+            if ax0 and done % reimpose_freq == 0:
+                self._impose(ax0, done)
             started = done
             if tracker is not None and m > 0 and done == next_check and done < max_steps:
                 next_check += m

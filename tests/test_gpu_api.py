@@ -476,6 +476,25 @@ class TestSlabEngine:
         assert [c.r_rms for c in par.checks] == [c.r_rms for c in serial.checks]
         assert par.halo_messages == 2 * (workers - 1) * 120
 
+    @pytest.mark.parametrize("workers", [2, 4])
+    def test_fixed_recipe_axis0_parity_native(self, gpu_lib, workers):
+        """The C3 recipe shape on slabs: fixed steps, observables and
+        renormalisation every m, antisymmetry along the slab axis re-imposed
+        every m through the mirror exchange between native segments; bitwise
+        the single-slab evolve_fixed."""
+        n = 24 if workers == 2 else 32
+        spec = LatticeSpec(N=n, a=0.5, m=1.0, dtau=0.0625)
+        grid = harmonic(spec)
+        c = SymmetryConstraint("x", "antisymmetric")
+        init = project(fill_random_gaussian(allocate(spec), 13), c)
+        ref = evolve_fixed(init, grid, 90, 30, norm_every=30, constraints=[c],
+                           reimpose_every=30)
+        par = evolve_parallel(grid, workers=workers, initial=init, check_freq=30, max_steps=90,
+                              max_snapshots=0, norm_every=30, fixed=True, constraints=[c],
+                              reimpose_freq=30)
+        assert np.array_equal(par.psi.values, ref.psi.values)
+        assert [k.energy for k in par.checks] == [k.energy for k in ref.checks]
+
     def test_parity_across_slabs(self, gpu_lib):
         spec = LatticeSpec(N=12, a=0.5, m=1.0, dtau=0.0625)
         grid = harmonic(spec)
