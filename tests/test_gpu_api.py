@@ -590,3 +590,23 @@ def test_bootstrap_resident_matches_host_path(gpu_lib, monkeypatch):
     assert np.array_equal(resident.psi.values, host.psi.values)
     assert [r.iterations for r in resident.stage_reports] == [r.iterations for r in host.stage_reports]
     assert [c.energy for c in resident.checks] == [c.energy for c in host.checks]
+
+
+def test_convergence_with_sparse_normalisation(gpu_lib):
+    """evolve_to_convergence(norm_every=k): renormalising every k-th sweep
+    (two-sweep passes in between) stays within roundoff of the reference's
+    per-sweep normalisation: same stopping step, E and r_rms to 1e-12, field
+    to 1e-12 of its maximum."""
+    spec = LatticeSpec(N=100, a=0.12, m=1.0, dtau=0.12 * 0.12 / 4.0)
+    grid = harmonic(spec)
+    init = fill_random_gaussian(allocate(spec), 21)
+    ref = evolve_to_convergence(init, grid, tol=1e-6, check_freq=50, max_steps=2000,
+                                max_snapshots=0)
+    fast = evolve_to_convergence(init, grid, tol=1e-6, check_freq=50, max_steps=2000,
+                                 max_snapshots=0, norm_every=50)
+    assert fast.step_count == ref.step_count and fast.converged == ref.converged
+    for a, b in zip(fast.checks, ref.checks):
+        assert abs(a.energy - b.energy) <= 1e-12 * abs(b.energy)
+        assert abs(a.r_rms - b.r_rms) <= 1e-12 * abs(b.r_rms)
+    d = np.max(np.abs(fast.psi.values - ref.psi.values))
+    assert d <= 1e-12 * np.max(np.abs(ref.psi.values))
