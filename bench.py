@@ -213,7 +213,7 @@ def run_reference(args):
     line = {
         "metric": "fp64 FDTD lattice-site updates/s (GLUPS)", "value": glups, "unit": "GLUPS",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
+        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": w.name, "N": n, "a": spec.a, "dtau": spec.dtau,
                    "measure_every": w.measure_every},
@@ -340,7 +340,7 @@ def run_single(args):
         "metric": "fp64 FDTD lattice-site updates/s (GLUPS)",
         "value": value, "unit": "GLUPS", "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": w.name, "N": n, "a": spec.a, "dtau": spec.dtau,
                    "potential": w.potential, "measure_every": m, "norm_every": m,
                    "l2": "inputs (3 x %.0f MB) larger than L2; no flush" % (ext ** 3 * 8 / 1e6),
