@@ -316,6 +316,8 @@ def run_single(args):
     traffic = load_traffic(n, "k_sweep2b" if two_step else "k_sweep")
     kname = ("k_sweep2b (two fp64 7-point sweeps per HBM pass, TMA z-march)" if two_step
              else "k_sweep (fp64 7-point, TMA z-march)")
+    npass, nsingle = t2_schedule(args.steps, args.warmup, m)
+    share = ((npass if two_step else args.steps) * kernel_s) / (ms * 1e-3)
 
     # ---- e2e through the public API from pinned host buffers ----
     grid = PotentialGrid(spec=spec, v=vhost, v_inf=0.0, unbounded=False, name="custom")
@@ -350,7 +352,10 @@ def run_single(args):
                      "kernel": kname,
                      "kernel_us": kernel_s * 1e6, "peak_source": peak_kind,
                      "algorithmic_bytes_per_launch": BYTES_PER_SITE * n ** 3,
-                     "site_updates_per_launch": (2 if two_step else 1) * n ** 3},
+                     "site_updates_per_launch": (2 if two_step else 1) * n ** 3,
+                     # launches of this kernel in the timed region x its mean duration, over
+                     # the region's time (the committed ncu launch list gives its share too)
+                     "share_of_timed_region": share},
         "clocks": clocks,
         "e2e": {"value": e2e, "unit": "GLUPS", "h2d_bytes_per_step": h2d / args.steps,
                 "d2h_bytes_per_step": d2h / args.steps,
@@ -363,6 +368,32 @@ def run_single(args):
                         if len(sums) else None},
     }
     print(json.dumps(line), flush=True)
+
+
+def t2_schedule(steps: int, offset: int, m: int):
+    """(two-sweep passes, single sweeps) psg_run issues for a fixed run with
+    measure / norm every m (the pairing rule of run_loop in csrc/psigpu.cu:
+    runs of plain steps go in pairs; a step carrying a pending factor is single)."""
+    def plain(t):
+        sidx = offset + t
+        meas = m > 0 and sidx - 1 > 0 and (sidx - 1) % m == 0
+        norm = m > 0 and sidx % m == 0
+        return not meas and not norm
+
+    t, pending, passes, singles = 1, False, 0, 0
+    while t <= steps:
+        if not pending and plain(t):
+            run = 1
+            while t + run <= steps and plain(t + run):
+                run += 1
+            if run >= 2:
+                passes += run // 2
+                t += 2 * (run // 2)
+                continue
+        pending = m > 0 and (offset + t) % m == 0
+        singles += 1
+        t += 1
+    return passes, singles
 
 
 def weak_n(n1: int, m: int) -> int:
