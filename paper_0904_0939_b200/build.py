@@ -29,7 +29,10 @@ def nvcc() -> str:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
-    deps = [SRC, os.path.join(HERE, "..", "include", "psigpu.h")]
+    csrc = os.path.join(HERE, "csrc")
+    deps = [os.path.join(csrc, f) for f in sorted(os.listdir(csrc))
+            if f.endswith((".cu", ".cuh"))]
+    deps.append(os.path.join(HERE, "..", "include", "psigpu.h"))
     if not force and os.path.exists(OUT) and all(
             os.path.getmtime(OUT) >= os.path.getmtime(d) for d in deps):
         return OUT

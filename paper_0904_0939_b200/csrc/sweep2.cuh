@@ -1,0 +1,436 @@
+// sweep2.cuh -- k_sweep2b: two sweeps per HBM pass (temporal blocking).
+// Part of the single translation unit csrc/psigpu.cu (included there, inside its
+// anonymous namespace; the host engine instantiates the templates).
+#pragma once
+
+// ------------------------------------------------------------------
+// two sweeps per pass (temporal blocking, k_sweep2b): plain steps s, s+1 of
+// the update in one march over z, so HBM sees one read of psi and V and one
+// write of psi for two site-updates.  Step 1 runs on the tile plus a one-site
+// ring (tile rows +-1 and the columns either side) into a shared-memory ring
+// of psi' planes; step 2 updates the tile from it one plane behind, with A and
+// C formed once per site in step 1 and kept in registers.  Per-site
+// arithmetic is k_sweep's: results are bitwise those of two k_sweep launches.
+// The kernel is issue-bound rather than DRAM-bound, so the code is written
+// for instruction count: warp roles are split at block entry into straight-
+// line loops, the plane loop is unrolled by three so the centre / psi' / A / C
+// registers rotate by renaming, shared memory is addressed by 32-bit offsets
+// with immediates and the output pointer advances by one plane stride.
+// ------------------------------------------------------------------
+__device__ __forceinline__ double2 lds2_u(uint32_t a) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ double lds1_u(uint32_t a) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts2_u(uint32_t a, double2 v) {
+  asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.x), "d"(v.y) : "memory");
+}
+__device__ __forceinline__ void sts1_u(uint32_t a, double v) {
+  asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_u(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// the retry loop (with the watchdog) out of line: the hot path is one
+// try_wait and a branch
+__device__ __noinline__ void mbar_wait_slow(uint32_t bar, uint32_t parity) {
+  uint32_t spins = 0;
+  while (!mbar_try_u(bar, parity)) {
+    if (++spins > (1u << 24)) __trap();
+  }
+}
+__device__ __forceinline__ void mbar_wait_u(uint32_t bar, uint32_t parity) {
+  if (!mbar_try_u(bar, parity)) mbar_wait_slow(bar, parity);
+}
+__device__ __forceinline__ void mbar_arrive_u(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+
+// pipeline cursor over the TMA stages (consumer side)
+template <int S>
+struct StageCursor {
+  int slot = 0;
+  uint32_t ph = 0;
+  __device__ __forceinline__ void next() {
+    if (++slot == S) {
+      slot = 0;
+      ph ^= 1u;
+    }
+  }
+};
+
+struct T2Item {
+  int z0, z1, j, k, idx;
+};
+
+// Tile of TB rows (8 or 16) x 64 columns.  Consumer warp w < TB+2 owns E row
+// w (psi' rows j0-1 .. j0+TB; columns k0+2l, k0+2l+1); warps 1..TB (STEP2)
+// also update their two tile sites one plane behind; warp TB+2 computes the
+// ring columns k0-1 / k0+64 of rows j0 .. j0+TB-1 (lane l < 2 TB: one site).
+// The psi' planes go through a ring of 4 slots: warp w publishes plane g with
+// an arrive on rfull[g % 4] and, before step 2 of plane g-1, waits for
+// rfull[(g-1) % 4], so warps drift by up to one plane instead of meeting at a
+// block barrier.  Slot g % 4 is rewritten at g+4, after the writer has seen
+// rfull(g+2), i.e. after every warp finished the step 2 that read plane g.
+constexpr int T2B_RS = 4;
+template <int TB>
+struct T2BGeo {
+  static constexpr int CW = TB + 3;                     // consumer warps
+  static constexpr int THREADS = 32 * (CW + 1);
+  static constexpr int MINB = TB <= 8 ? 2 : 1;
+  static constexpr int PSI_H = TB + 4;                  // psi rows j0-2 .. j0+TB+1
+  static constexpr int PSI_BYTES = BOXW * PSI_H * 8;
+  static constexpr int PSI_STRIDE = (PSI_BYTES + 127) / 128 * 128;
+  static constexpr int VH = TB + 2;                     // V rows j0-1 .. j0+TB
+  static constexpr int V_BYTES = BOXW * VH * 8;
+  static constexpr int V_STRIDE = (V_BYTES + 127) / 128 * 128;
+  static constexpr int STAGE = PSI_STRIDE + V_STRIDE;
+  static constexpr int RING = BOXW * VH * 8;            // bytes per psi' plane
+};
+template <int NST, int TB, int RS = T2B_RS>
+struct T2BCfg {
+  using G = T2BGeo<TB>;
+  static constexpr int RING_OFF = NST * G::STAGE;
+  static constexpr int BAR_OFF = RING_OFF + RS * G::RING;
+  static constexpr int SMEM = BAR_OFF + (2 * NST + RS) * 8;
+};
+
+template <int TB>
+__device__ __forceinline__ T2Item t2b_item(const SweepArgs& a, int item) {
+  int chunk = item / a.tiles;
+  const int tile = item - chunk * a.tiles;
+  const int tj = tile / a.tiles_k;
+  const int tk = tile - tj * a.tiles_k;
+  T2Item r;
+  r.idx = item;
+  if (a.corder > 0) {
+    // edges first: 0, nch-1 (, nch-2), then 1, 2, ...
+    const int nch = a.nchunks;
+    if (chunk == 1) chunk = nch - 1;
+    else if (chunk == 2 && a.corder == 3) chunk = nch - 2;
+    else if (chunk > 0) chunk = chunk - (a.corder - 1);
+  } else if (a.reverse) {
+    chunk = a.nchunks - 1 - chunk;
+  }
+  chunk_range(a, chunk, r.z0, r.z1);
+  r.j = 1 + tj * TB;
+  r.k = 1 + tk * TX;
+  return r;
+}
+
+// a work item whose step-1 region (tile rows j0-1 .. j0+TB, columns k0-1 ..
+// k0+64, global planes x_off+z0-1 .. x_off+z1+1) lies inside the lattice
+// needs no site masks
+template <int TB>
+__device__ __forceinline__ bool t2b_interior(const T2Item& I, int n, int x_off) {
+  return (I.j >= 2) & (I.j + TB <= n) & (I.k >= 2) & (I.k + TX <= n) & (x_off + I.z0 >= 2) &
+         (x_off + I.z1 < n);
+}
+
+
+// one work item of an E-row warp (MASK: item touches the lattice boundary)
+template <int S, int TB, bool STEP2, bool FASTC, bool MASK>
+__device__ __forceinline__ void t2b_rows_item(const SweepArgs& args, const T2Item& I,
+                                              uint32_t fb, uint32_t base, int w, int lane,
+                                              StageCursor<S>& nx, uint32_t& g) {
+  using G = T2BGeo<TB>;
+  using C = T2BCfg<S, TB>;
+  constexpr uint32_t VOFF = G::PSI_STRIDE - BOXW * 8;  // V box starts one row lower
+  constexpr uint32_t ROFF = C::RING_OFF - BOXW * 8;    // ring holds E rows
+  const int n = args.n;
+  const double h = args.h, c0 = args.c0;
+  const int j = I.j - 1 + w;
+  const int k = I.k + 2 * lane;
+  const bool in_j = (unsigned)(j - 1) < (unsigned)n;
+  const bool in0 = in_j & (k <= n);
+  const bool in1 = in_j & (k + 1 <= n);
+  const bool ok0 = (j <= n) & (k <= n);
+  const bool ok1 = (j <= n) & (k + 1 <= n);
+  // element offset of this lane's output pair (fields < 2^32 elements, checked
+  // on the host): one 32-bit add per plane instead of 64-bit pointer math
+  uint32_t doff = (uint32_t)((long long)(I.z0 - 2) * args.plane_stride + (long long)j * args.pitch +
+                             (k + COL_OFF));
+  const uint32_t pstride = (uint32_t)args.plane_stride;
+  // ring slot byte offsets of planes g (write) and g-1 (read), and the rfull
+  // barrier of slot g, rotating mod 4
+  uint32_t rw = (g & 3u) * G::RING, rr = ((g - 1) & 3u) * G::RING;
+  constexpr uint32_t RB_END = 4 * G::RING;
+  mbar_wait_u(fb + nx.slot * 8, nx.ph);
+  double2 c_a = lds2_u(base + nx.slot * G::STAGE);
+  mbar_arrive_u(fb + (S + nx.slot) * 8);   // every lane arrives (count 32 per warp)
+  nx.next();
+  mbar_wait_u(fb + nx.slot * 8, nx.ph);
+  double2 c_b = lds2_u(base + nx.slot * G::STAGE);
+  int cur = nx.slot;
+  nx.next();
+  double2 c_c;
+  double2 q0 = make_double2(0.0, 0.0), q1 = q0, q2 = q0;
+  double2 a0 = q0, a1 = q0, a2 = q0, f0 = q0, f1 = q0, f2 = q0;
+  const int pend = I.z1 + 2;
+  int p = I.z0 - 1;
+  auto plane = [&](const double2& cp, const double2& cc, double2& cn, double2& qw,
+                   const double2& qm, const double2& qmm, double2& aw, double2& fw,
+                   const double2& am, const double2& fm) {
+    mbar_wait_u(fb + nx.slot * 8, nx.ph);
+    cn = lds2_u(base + nx.slot * G::STAGE);
+    const uint32_t sc = base + cur * G::STAGE;
+    const double2 jm = lds2_u(sc - BOXW * 8);
+    const double2 jp = lds2_u(sc + BOXW * 8);
+    const double km = lds1_u(sc - 8);
+    const double kp = lds1_u(sc + 16);
+    const double2 v = lds2_u(sc + VOFF);
+    coef2<FASTC>(v, h, c0, aw.x, fw.x, aw.y, fw.y);
+    const double u0 = upd(aw.x, fw.x, cc.x, cp.x, cn.x, jm.x, jp.x, km, cc.y);
+    const double u1 = upd(aw.y, fw.y, cc.y, cp.y, cn.y, jm.y, jp.y, cc.x, kp);
+    if (MASK) {
+      const bool pin = (unsigned)(args.x_off + p - 1) < (unsigned)n;   // global plane
+      qw.x = (pin & in0) ? u0 : cc.x;
+      qw.y = (pin & in1) ? u1 : cc.y;
+    } else {
+      qw = make_double2(u0, u1);
+    }
+    sts2_u(base + ROFF + rw, qw);
+    mbar_arrive_u(fb + (S + cur) * 8);
+    mbar_arrive_u(fb + (2 * S + (g & 3u)) * 8);
+    cur = nx.slot;
+    nx.next();
+    if (g > 0) {
+      const uint32_t gp = g - 1;
+      mbar_wait_u(fb + (2 * S + (gp & 3u)) * 8, (gp >> 2) & 1u);
+      if (STEP2) {
+        const uint32_t rq = base + ROFF + rr;
+        const double2 rjm = lds2_u(rq - BOXW * 8);
+        const double2 rjp = lds2_u(rq + BOXW * 8);
+        const double rkm = lds1_u(rq - 8);
+        const double rkp = lds1_u(rq + 16);
+        const double o0 = upd(am.x, fm.x, qm.x, qmm.x, qw.x, rjm.x, rjp.x, rkm, qm.y);
+        const double o1 = upd(am.y, fm.y, qm.y, qmm.y, qw.y, rjm.y, rjp.y, qm.x, rkp);
+        if (p > I.z0) {   // plane p-1 >= z0
+          double* dst = args.out + doff;
+          if (!MASK || ok1) {
+            *reinterpret_cast<double2*>(dst) = make_double2(o0, o1);
+          } else if (ok0) {
+            *dst = o0;
+          }
+        }
+      }
+    }
+    if (STEP2) doff += pstride;
+    rr = rw;
+    rw = rw + G::RING == RB_END ? 0u : rw + G::RING;
+    ++p;
+    ++g;
+  };
+  for (;;) {
+    plane(c_a, c_b, c_c, q0, q2, q1, a0, f0, a2, f2);
+    if (p == pend) break;
+    plane(c_b, c_c, c_a, q1, q0, q2, a1, f1, a0, f0);
+    if (p == pend) break;
+    plane(c_c, c_a, c_b, q2, q1, q0, a2, f2, a1, f1);
+    if (p == pend) break;
+  }
+  mbar_arrive_u(fb + (S + cur) * 8);
+  if (STEP2 && I.idx < args.sig_items) {
+    // an edge item's planes are stored: make them visible, then count this
+    // warp done (the exchange waits for the count on its own stream)
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) atomicAdd(args.sig, 1ull);
+  }
+}
+
+template <int S, int TB, bool STEP2, bool FASTC>
+__device__ __forceinline__ void t2b_rows(const SweepArgs& args, uint32_t sm0, int w, int lane) {
+  using C = T2BCfg<S, TB>;
+  const uint32_t fb = sm0 + C::BAR_OFF;               // full[S], empty[S], rfull[4]
+  const uint32_t base = sm0 + (uint32_t)(((w + 1) * BOXW + 2 * lane + 2) * 8);
+  StageCursor<S> nx;
+  uint32_t g = 0;   // ring plane counter (runs across items)
+  for (int item = blockIdx.x; item < args.nitems; item += gridDim.x) {
+    const T2Item I = t2b_item<TB>(args, item);
+    if (t2b_interior<TB>(I, args.n, args.x_off))
+      t2b_rows_item<S, TB, STEP2, FASTC, false>(args, I, fb, base, w, lane, nx, g);
+    else
+      t2b_rows_item<S, TB, STEP2, FASTC, true>(args, I, fb, base, w, lane, nx, g);
+  }
+}
+
+template <int S, int TB, bool FASTC, bool MASK>
+__device__ __forceinline__ void t2b_ring_item(const SweepArgs& args, const T2Item& I, uint32_t fb,
+                                              uint32_t base, int rrow, int rcol, bool active,
+                                              int lane, StageCursor<S>& nx, uint32_t& g) {
+  using G = T2BGeo<TB>;
+  using C = T2BCfg<S, TB>;
+  constexpr uint32_t VOFF = G::PSI_STRIDE - BOXW * 8;
+  constexpr uint32_t ROFF = C::RING_OFF - BOXW * 8;
+  const int n = args.n;
+  const double h = args.h, c0 = args.c0;
+  const int j = I.j - 1 + rrow;
+  const int k = I.k - 2 + rcol;
+  const bool in0 = active & (j <= n) & ((unsigned)(k - 1) < (unsigned)n);
+  mbar_wait_u(fb + nx.slot * 8, nx.ph);
+  double c_a = lds1_u(base + nx.slot * G::STAGE);
+  mbar_arrive_u(fb + (S + nx.slot) * 8);   // every lane arrives (count 32 per warp)
+  nx.next();
+  mbar_wait_u(fb + nx.slot * 8, nx.ph);
+  double c_b = lds1_u(base + nx.slot * G::STAGE);
+  int cur = nx.slot;
+  nx.next();
+  double c_c;
+  const int pend = I.z1 + 2;
+  int p = I.z0 - 1;
+  auto plane = [&](const double& cp, const double& cc, double& cn) {
+    mbar_wait_u(fb + nx.slot * 8, nx.ph);
+    cn = lds1_u(base + nx.slot * G::STAGE);
+    const uint32_t sc = base + cur * G::STAGE;
+    const double jm = lds1_u(sc - BOXW * 8);
+    const double jp = lds1_u(sc + BOXW * 8);
+    const double km = lds1_u(sc - 8);
+    const double kp = lds1_u(sc + 8);
+    const double v = lds1_u(sc + VOFF);
+    double A, Cc;
+    coef1<FASTC>(v, h, c0, A, Cc);
+    const double u = upd(A, Cc, cc, cp, cn, jm, jp, km, kp);
+    double qv = u;
+    if (MASK) {
+      const bool pin = (unsigned)(args.x_off + p - 1) < (unsigned)n;   // global plane
+      qv = (pin & in0) ? u : cc;
+    }
+    if (active) sts1_u(base + ROFF + (g & 3u) * G::RING, qv);
+    mbar_arrive_u(fb + (S + cur) * 8);
+    mbar_arrive_u(fb + (2 * S + (g & 3u)) * 8);
+    cur = nx.slot;
+    nx.next();
+    if (g > 0) mbar_wait_u(fb + (2 * S + ((g - 1) & 3u)) * 8, ((g - 1) >> 2) & 1u);
+    ++p;
+    ++g;
+  };
+  for (;;) {
+    plane(c_a, c_b, c_c);
+    if (p == pend) break;
+    plane(c_b, c_c, c_a);
+    if (p == pend) break;
+    plane(c_c, c_a, c_b);
+    if (p == pend) break;
+  }
+  mbar_arrive_u(fb + (S + cur) * 8);
+}
+
+template <int S, int TB, bool FASTC>
+__device__ __forceinline__ void t2b_ringw(const SweepArgs& args, uint32_t sm0, int lane) {
+  using C = T2BCfg<S, TB>;
+  const uint32_t fb = sm0 + C::BAR_OFF;
+  const int rrow = 1 + (lane % TB);
+  const int rcol = lane < TB ? 1 : 66;
+  const bool active = lane < 2 * TB;
+  const uint32_t base = sm0 + (uint32_t)(((rrow + 1) * BOXW + rcol) * 8);
+  StageCursor<S> nx;
+  uint32_t g = 0;
+  for (int item = blockIdx.x; item < args.nitems; item += gridDim.x) {
+    const T2Item I = t2b_item<TB>(args, item);
+    if (t2b_interior<TB>(I, args.n, args.x_off))
+      t2b_ring_item<S, TB, FASTC, false>(args, I, fb, base, rrow, rcol, active, lane, nx, g);
+    else
+      t2b_ring_item<S, TB, FASTC, true>(args, I, fb, base, rrow, rcol, active, lane, nx, g);
+  }
+}
+
+template <int NST, int TB, bool FASTC>
+__global__ void __launch_bounds__(T2BGeo<TB>::THREADS, T2BGeo<TB>::MINB)
+    k_sweep2b(const __grid_constant__ CUtensorMap tm_psi, const __grid_constant__ CUtensorMap tm_v,
+              const SweepArgs args) {
+  using G = T2BGeo<TB>;
+  constexpr int RS = T2B_RS;
+  using C = T2BCfg<NST, TB, RS>;
+  constexpr int S = NST;
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
+  uint64_t* empty = full + S;
+  uint64_t* rfull = empty + S;
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], G::CW * 32);   // per-lane arrivals of the consumer warps
+    }
+    for (int r = 0; r < RS; ++r) mbar_init(&rfull[r], G::CW * 32);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  pdl_launch_dependents();
+  pdl_wait();
+  if (warp == G::CW) {
+    if (lane == 0) {
+      tma_prefetch_desc(&tm_psi);
+      tma_prefetch_desc(&tm_v);
+      int it = 0;
+      for (int item = blockIdx.x; item < args.nitems; item += gridDim.x) {
+        const T2Item I = t2b_item<TB>(args, item);
+        const int kc = I.k + COL_OFF;
+        for (int p = I.z0 - 2; p <= I.z1 + 2; ++p, ++it) {
+          const int slot = it % S;
+          if (it >= S) mbar_wait_sleep(&empty[slot], ((it / S) - 1) & 1);
+          const bool hasv = (p >= I.z0 - 1) && (p <= I.z1 + 1);
+          unsigned char* st = smem + slot * G::STAGE;
+          mbar_arrive_expect_tx(&full[slot], G::PSI_BYTES + (hasv ? G::V_BYTES : 0));
+          tma_load_3d(st, &tm_psi, kc - 2, I.j - 2, p + 1, &full[slot]);   // deep-halo map: plane + 1
+          // V without the evict-first hint here: neighbouring tiles re-read its halo
+          // rows / columns from L2 (-4 % DRAM bytes, +1..2 % at 256^3..512^3)
+          if (hasv) tma_load_3d(st + G::PSI_STRIDE, &tm_v, kc - 2, I.j - 1, p, &full[slot]);
+        }
+      }
+    }
+    return;
+  }
+  const uint32_t sm0 = smem_u32(smem);
+  if (warp == TB + 2) {
+    t2b_ringw<S, TB, FASTC>(args, sm0, lane);
+  } else if (warp == 0 || warp == TB + 1) {
+    t2b_rows<S, TB, false, FASTC>(args, sm0, warp, lane);
+  } else {
+    t2b_rows<S, TB, true, FASTC>(args, sm0, warp, lane);
+  }
+}
+
+// division self-test: compares coef_pair against IEEE division on random
+// potentials h*V in [lo, hi) (psg_selftest_division)
+__global__ void k_div_check(unsigned long long seed, long long count, double lo, double hi,
+                            unsigned long long* mismatches, int variant) {
+  unsigned long long bad = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
+       i += (long long)gridDim.x * blockDim.x) {
+    unsigned long long x = seed ^ (0x9E3779B97F4A7C15ull * (unsigned long long)(i + 1));
+    x ^= x >> 30; x *= 0xBF58476D1CE4E5B9ull; x ^= x >> 27; x *= 0x94D049BB133111EBull; x ^= x >> 31;
+    const double u = (double)(x >> 11) * 0x1.0p-53;
+    const double v = lo + u * (hi - lo);
+    double A, Cc;
+    if (variant) {
+      double A1, C1;
+      coef_pair2(make_double2(v, v), 1.0, 1.0, A, Cc, A1, C1);
+    } else {
+      coef_pair(v, 1.0, 1.0, A, Cc);
+    }
+    const double d = __dadd_rn(1.0, v);
+    const double Aw = __ddiv_rn(__dsub_rn(1.0, v), d);
+    const double Bw = __ddiv_rn(1.0, d);
+    if (__double_as_longlong(A) != __double_as_longlong(Aw) ||
+        __double_as_longlong(Cc) != __double_as_longlong(Bw))
+      ++bad;
+  }
+  if (bad) atomicAdd(mismatches, bad);
+}

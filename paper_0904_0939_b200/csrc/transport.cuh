@@ -1,0 +1,482 @@
+// transport.cuh -- slab transports (NCCL, peer copies) and the fused fixed-step run loop.
+// Part of the single translation unit csrc/psigpu.cu (included there, inside its
+// anonymous namespace, after the slab object it operates on).
+#pragma once
+
+// ------------------------------------------------------------------
+// slab transports.  A z-decomposed run moves halo planes between neighbouring
+// slabs and sums the zero-padded plane-sum vectors; the loop below is the same
+// for NCCL ranks (one slab per process) and for several slabs driven by one
+// process (peer copies over NVLink, or plain copies on one device).
+//   post(depth): enqueue the exchange of `depth` planes per face (after each
+//                slab's previous work) on the slabs' communication streams
+//   wait():      order each slab's main stream after its halo arrival
+//   allreduce(): after every slab's reduce, every slab holds the global sums
+// Every cross-stream dependency is an event; nothing spins on the device.
+// ------------------------------------------------------------------
+struct Transport {
+  bool deep = false;   // two halo planes per face of every slab's current buffer are posted
+  virtual ~Transport() {}
+  virtual bool has_left(size_t r) const = 0;
+  virtual bool has_right(size_t r) const = 0;
+  virtual int post(int depth) = 0;
+  // exchange of the OUTPUT buffers' edge planes of the pass just launched,
+  // started on the device's signal that the slab's edge items are stored
+  // (slab counter >= its sig_target) instead of after the whole pass
+  virtual int post_signal(int depth) = 0;
+  virtual int wait() = 0;
+  virtual int allreduce() = 0;
+};
+
+struct NcclTransport : Transport {
+  psg_slab* s;
+  psg_comm* c;
+  int left, right;
+  bool posted = false;
+  NcclTransport(psg_slab* s_, psg_comm* c_, int l, int r) : s(s_), c(c_), left(l), right(r) {}
+  bool has_left(size_t) const override { return left >= 0; }
+  bool has_right(size_t) const override { return right >= 0; }
+  int post(int depth) override { return exchange(depth, false); }
+  int post_signal(int depth) override { return exchange(depth, true); }
+  int exchange(int depth, bool signal) {
+    posted = false;
+    if (left < 0 && right < 0) return PSG_OK;
+    NcclApi* api = nccl();
+    const size_t ps = (size_t)s->plane_stride;
+    const size_t cnt = (size_t)depth * ps;
+    double* cur = s->psi[signal ? 1 - s->cur : s->cur];
+    const int64_t w = s->w;
+    if (signal) {
+      int rc = stream_wait_value(c->cstream, s->sig_dev, s->sig_target);
+      if (rc) return rc;
+    } else {
+      CU_TRY(cudaEventRecord(c->ev_main, s->stream));
+      CU_TRY(cudaStreamWaitEvent(c->cstream, c->ev_main, 0));
+    }
+    NCCL_TRY(api->GroupStart());
+    if (left >= 0) {   // planes 1..depth -> left's W+1..; left's W-depth+1..W -> 1-depth..0
+      NCCL_TRY(api->Send(cur + ps, cnt, ncclFloat64, left, c->comm, c->cstream));
+      NCCL_TRY(api->Recv(cur + ps - cnt, cnt, ncclFloat64, left, c->comm, c->cstream));
+    }
+    if (right >= 0) {
+      NCCL_TRY(api->Send(cur + (size_t)(w + 1) * ps - cnt, cnt, ncclFloat64, right, c->comm, c->cstream));
+      NCCL_TRY(api->Recv(cur + (size_t)(w + 1) * ps, cnt, ncclFloat64, right, c->comm, c->cstream));
+    }
+    NCCL_TRY(api->GroupEnd());
+    CU_TRY(cudaEventRecord(c->ev_comm, c->cstream));
+    posted = true;
+    return PSG_OK;
+  }
+  int wait() override {
+    if (posted) CU_TRY(cudaStreamWaitEvent(s->stream, c->ev_comm, 0));
+    return PSG_OK;
+  }
+  int allreduce() override {
+    if (c->nranks > 1)
+      NCCL_TRY(nccl()->AllReduce(s->plane_sums, s->plane_sums, (size_t)NQ * s->n, ncclFloat64,
+                                 ncclSum, c->comm, s->stream));
+    return PSG_OK;
+  }
+};
+
+__global__ void k_add(double* __restrict__ out, const double* __restrict__ in, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    out[i] = __dadd_rn(out[i], in[i]);
+}
+
+struct LocalTransport : Transport {
+  std::vector<psg_slab*> sl;
+  std::vector<cudaStream_t> cs;
+  std::vector<cudaEvent_t> evm, evc, evr;
+  double* tmp0 = nullptr;   // on slab 0's device: one incoming plane-sum vector
+  ~LocalTransport() override {
+    for (size_t r = 0; r < sl.size(); ++r) {
+      cudaSetDevice(sl[r]->device);
+      if (r < cs.size() && cs[r]) cudaStreamSynchronize(cs[r]);
+      if (r < cs.size() && cs[r]) cudaStreamDestroy(cs[r]);
+      if (r < evm.size() && evm[r]) cudaEventDestroy(evm[r]);
+      if (r < evc.size() && evc[r]) cudaEventDestroy(evc[r]);
+      if (r < evr.size() && evr[r]) cudaEventDestroy(evr[r]);
+    }
+    if (tmp0) {
+      cudaSetDevice(sl[0]->device);
+      cudaFree(tmp0);
+    }
+  }
+  int init(psg_slab** slabs, int m) {
+    sl.assign(slabs, slabs + m);
+    cs.assign(m, nullptr);
+    evm.assign(m, nullptr);
+    evc.assign(m, nullptr);
+    evr.assign(m, nullptr);
+    for (int r = 0; r < m; ++r) {
+      CU_TRY(cudaSetDevice(sl[r]->device));
+      CU_TRY(cudaStreamCreateWithFlags(&cs[r], cudaStreamNonBlocking));
+      CU_TRY(cudaEventCreateWithFlags(&evm[r], cudaEventDisableTiming));
+      CU_TRY(cudaEventCreateWithFlags(&evc[r], cudaEventDisableTiming));
+      CU_TRY(cudaEventCreateWithFlags(&evr[r], cudaEventDisableTiming));
+    }
+    CU_TRY(cudaSetDevice(sl[0]->device));
+    CU_TRY(cudaMalloc(&tmp0, (size_t)NQ * sl[0]->n * sizeof(double)));
+    return PSG_OK;
+  }
+  bool has_left(size_t r) const override { return r > 0; }
+  bool has_right(size_t r) const override { return r + 1 < sl.size(); }
+  bool pushed = false;   // last exchange pushed by the source slabs (post_signal)
+  int post(int depth) override {
+    const size_t m = sl.size();
+    pushed = false;
+    if (m < 2) return PSG_OK;
+    for (size_t r = 0; r < m; ++r) {
+      CU_TRY(cudaSetDevice(sl[r]->device));
+      CU_TRY(cudaEventRecord(evm[r], sl[r]->stream));
+    }
+    for (size_t r = 0; r < m; ++r) {
+      psg_slab* s = sl[r];
+      CU_TRY(cudaSetDevice(s->device));
+      const size_t ps = (size_t)s->plane_stride;
+      const size_t bytes = (size_t)depth * ps * sizeof(double);
+      double* cur = s->psi[s->cur];
+      CU_TRY(cudaStreamWaitEvent(cs[r], evm[r], 0));
+      if (r > 0) {   // left neighbour's last planes -> my planes 1-depth .. 0
+        psg_slab* o = sl[r - 1];
+        CU_TRY(cudaStreamWaitEvent(cs[r], evm[r - 1], 0));
+        CU_TRY(cudaMemcpyPeerAsync(cur + ps - (size_t)depth * ps, s->device,
+                                   o->psi[o->cur] + (size_t)(o->w + 1 - depth) * ps, o->device,
+                                   bytes, cs[r]));
+      }
+      if (r + 1 < m) {   // right neighbour's first planes -> my planes W+1 .. W+depth
+        psg_slab* o = sl[r + 1];
+        CU_TRY(cudaStreamWaitEvent(cs[r], evm[r + 1], 0));
+        CU_TRY(cudaMemcpyPeerAsync(cur + (size_t)(s->w + 1) * ps, s->device, o->psi[o->cur] + ps,
+                                   o->device, bytes, cs[r]));
+      }
+      CU_TRY(cudaEventRecord(evc[r], cs[r]));
+    }
+    return PSG_OK;
+  }
+  // push model: when slab r's edge items are stored (its counter), copy its new
+  // edge planes into the neighbours' output-buffer halos (copy engines: no SMs)
+  int post_signal(int depth) override {
+    const size_t m = sl.size();
+    pushed = true;
+    if (m < 2) return PSG_OK;
+    for (size_t r = 0; r < m; ++r) {
+      psg_slab* s = sl[r];
+      CU_TRY(cudaSetDevice(s->device));
+      const size_t ps = (size_t)s->plane_stride;
+      const size_t bytes = (size_t)depth * ps * sizeof(double);
+      const double* out = s->psi[1 - s->cur];
+      int rc = stream_wait_value(cs[r], s->sig_dev, s->sig_target);
+      if (rc) return rc;
+      if (r > 0) {   // my planes 1..depth -> left's W+1 ..
+        psg_slab* o = sl[r - 1];
+        CU_TRY(cudaMemcpyPeerAsync(o->psi[1 - o->cur] + (size_t)(o->w + 1) * ps, o->device,
+                                   out + ps, s->device, bytes, cs[r]));
+      }
+      if (r + 1 < m) {   // my planes W-depth+1..W -> right's 1-depth .. 0
+        psg_slab* o = sl[r + 1];
+        CU_TRY(cudaMemcpyPeerAsync(o->psi[1 - o->cur] + ps - (size_t)depth * ps, o->device,
+                                   out + (size_t)(s->w + 1 - depth) * ps, s->device, bytes, cs[r]));
+      }
+      CU_TRY(cudaEventRecord(evc[r], cs[r]));
+    }
+    return PSG_OK;
+  }
+  int wait() override {
+    const size_t m = sl.size();
+    if (m < 2) return PSG_OK;
+    for (size_t r = 0; r < m; ++r) {
+      CU_TRY(cudaSetDevice(sl[r]->device));
+      if (pushed) {   // my halos were written by my neighbours' streams
+        if (r > 0) CU_TRY(cudaStreamWaitEvent(sl[r]->stream, evc[r - 1], 0));
+        if (r + 1 < m) CU_TRY(cudaStreamWaitEvent(sl[r]->stream, evc[r + 1], 0));
+      } else {
+        CU_TRY(cudaStreamWaitEvent(sl[r]->stream, evc[r], 0));
+      }
+    }
+    return PSG_OK;
+  }
+  int allreduce() override {
+    const size_t m = sl.size();
+    if (m < 2) return PSG_OK;
+    psg_slab* s0 = sl[0];
+    const size_t cnt = (size_t)NQ * s0->n;
+    for (size_t r = 1; r < m; ++r) {
+      CU_TRY(cudaSetDevice(sl[r]->device));
+      CU_TRY(cudaEventRecord(evr[r], sl[r]->stream));
+    }
+    // slab 0 gathers (one non-zero contributor per slot: exact in any order)
+    CU_TRY(cudaSetDevice(s0->device));
+    for (size_t r = 1; r < m; ++r) {
+      CU_TRY(cudaStreamWaitEvent(s0->stream, evr[r], 0));
+      CU_TRY(cudaMemcpyPeerAsync(tmp0, s0->device, sl[r]->plane_sums, sl[r]->device,
+                                 cnt * sizeof(double), s0->stream));
+      k_add<<<std::min<int>(1024, (int)((cnt + 255) / 256)), 256, 0, s0->stream>>>(s0->plane_sums,
+                                                                                 tmp0, (int)cnt);
+      CU_TRY(cudaGetLastError());
+    }
+    CU_TRY(cudaEventRecord(evr[0], s0->stream));
+    // and hands the total back
+    for (size_t r = 1; r < m; ++r) {
+      CU_TRY(cudaSetDevice(sl[r]->device));
+      CU_TRY(cudaStreamWaitEvent(sl[r]->stream, evr[0], 0));
+      CU_TRY(cudaMemcpyPeerAsync(sl[r]->plane_sums, sl[r]->device, s0->plane_sums, s0->device,
+                                 cnt * sizeof(double), sl[r]->stream));
+    }
+    return PSG_OK;
+  }
+};
+
+// edge / interior plane ranges of slab r for a halo depth (1: single sweep,
+// 2: two-sweep pass)
+inline void split_ranges(const psg_slab* s, bool l, bool r, int depth, int64_t& lo, int64_t& hi) {
+  lo = l ? 1 + depth : 1;
+  hi = r ? s->w - depth : s->w;
+}
+
+
+// one sweep of every slab: exchange one halo plane per face (overlapped with
+// the interior planes; nothing to post if the deep halos of the current
+// buffers are already in flight), then the edge planes
+int multi_sweep(std::vector<psg_slab*>& sl, Transport* tr, unsigned flags, bool write) {
+  int rc = tr->deep ? PSG_OK : tr->post(1);
+  if (rc) return rc;
+  for (size_t r = 0; r < sl.size(); ++r) {
+    CU_TRY(cudaSetDevice(sl[r]->device));
+    int64_t lo, hi;
+    split_ranges(sl[r], tr->has_left(r), tr->has_right(r), 1, lo, hi);
+    if (lo <= hi) rc = do_sweep(sl[r], lo, hi, flags, write);
+    if (rc) return rc;
+  }
+  rc = tr->wait();
+  if (rc) return rc;
+  for (size_t r = 0; r < sl.size(); ++r) {
+    psg_slab* s = sl[r];
+    CU_TRY(cudaSetDevice(s->device));
+    const bool l = tr->has_left(r), rr = tr->has_right(r);
+    if (l) rc = do_sweep(s, 1, 1, flags, write);
+    if (!rc && rr && (s->w > 1 || !l)) rc = do_sweep(s, s->w, s->w, flags, write);
+    if (rc) return rc;
+  }
+  tr->deep = false;
+  return PSG_OK;
+}
+
+// two sweeps of every slab in one pass each (k_sweep2b), pipelined so that
+// the halo exchange hides behind the interior, all on the slab's stream:
+//   the edge pairs 1..2 / W-1..W first (one launch), once the deep halos (two
+//   planes per face: local -1, 0 / W+1, W+2) of the current state are in;
+//   then the exchange for the NEXT pass is posted (it sends the edge planes
+//   just written and lands in the output buffer's halos) and runs while
+//   the interior planes 3..W-2 are updated.
+// One exchange per two sweeps; cross-stream ordering by events only.
+// two sweeps of every slab in one pass each (k_sweep2b): ONE launch per slab
+// whose chunk order puts the edge planes (1..2, W-1..W) first; as the step-2
+// warps of those items store, they count on the slab's device counter, and
+// the exchange of the new edge planes (the next pass's deep halos) is queued
+// on the communication stream behind a wait for that count
+// (cuStreamWaitValue64), so it runs while the launch is still updating the
+// interior.  One exchange per two sweeps; no host in the loop.
+int multi_sweep2(std::vector<psg_slab*>& sl, Transport* tr) {
+  int rc = tr->deep ? PSG_OK : tr->post(2);
+  if (rc) return rc;
+  rc = tr->wait();
+  if (rc) return rc;
+  for (psg_slab* s : sl) {
+    CU_TRY(cudaSetDevice(s->device));
+    if (!s->sig_dev) {
+      // plain device allocation: stream memory operations do not accept pool memory
+      if (cudaMalloc((void**)&s->sig_dev, sizeof(unsigned long long)) != cudaSuccess)
+        return fail(PSG_ERR_CUDA, "signal counter allocation failed");
+      CU_TRY(cudaMemsetAsync(s->sig_dev, 0, sizeof(unsigned long long), s->stream));
+      s->sig_target = 0;
+    }
+    rc = pass2(s, 1, s->w, true);
+    if (rc) return rc;
+  }
+  rc = tr->post_signal(2);
+  if (rc) return rc;
+  tr->deep = true;
+  for (psg_slab* s : sl) s->cur = 1 - s->cur;
+  return PSG_OK;
+}
+
+int ensure_hist(psg_slab* s, int64_t want) {
+  const int64_t rec = 3 * s->n + 2;
+  if (want > s->hist_cap) {
+    dev_free(s->hist_dev, s->stream);
+    s->hist_dev = nullptr;
+    if (dev_alloc((void**)&s->hist_dev, (size_t)want * rec * sizeof(double), s->stream))
+      return fail(PSG_ERR_CUDA, "history allocation failed");
+    s->hist_cap = want;
+  }
+  return PSG_OK;
+}
+
+// observables of the current state of every slab (halo exchange, measuring
+// pass, global sums, combine); slab 0's record (3n+2 doubles) to rec
+int measure_loop(std::vector<psg_slab*>& sl, Transport* tr, double* rec) {
+  int rc = PSG_OK;
+  for (psg_slab* s : sl) {
+    CU_TRY(cudaSetDevice(s->device));
+    rc = ensure_hist(s, 1);
+    if (rc) return rc;
+  }
+  rc = multi_sweep(sl, tr, PSG_F_MEASURE, false);
+  if (rc) return rc;
+  const unsigned q = qmask_of(PSG_F_MEASURE);
+  for (psg_slab* s : sl) {
+    CU_TRY(cudaSetDevice(s->device));
+    CU_TRY(cudaMemsetAsync(s->plane_sums, 0, (size_t)NQ * s->n * sizeof(double), s->stream));
+    rc = do_reduce(s, 1, s->w, q, false, nullptr);
+    if (rc) return rc;
+  }
+  rc = tr->allreduce();
+  if (rc) return rc;
+  for (psg_slab* s : sl) {
+    CU_TRY(cudaSetDevice(s->device));
+    rc = do_combine(s, q, s->hist_dev);
+    if (rc) return rc;
+  }
+  psg_slab* s0 = sl[0];
+  CU_TRY(cudaSetDevice(s0->device));
+  CU_TRY(cudaMemcpyAsync(rec, s0->hist_dev, (size_t)(3 * s0->n + 2) * sizeof(double),
+                         cudaMemcpyDeviceToHost, s0->stream));
+  for (psg_slab* s : sl) {
+    CU_TRY(cudaSetDevice(s->device));
+    CU_TRY(cudaStreamSynchronize(s->stream));
+  }
+  return PSG_OK;
+}
+
+// the fused fixed-step loop of psg_run / psg_run_dist / psg_run_multi
+// (evolve.py:249-270, parallel.py:413-485): sweeps with their fused
+// reductions, the combine (after the sum of the zero-padded plane-sum vectors
+// for slabs), the factor folded into the next sweep, re-imposition; pairs of
+// plain steps go through the two-sweep pass.  No host round trip until the
+// end.  tr == nullptr: one whole-lattice slab.
+int run_loop(std::vector<psg_slab*>& sl, Transport* tr, const psg_run_params* p, double* hist,
+             int64_t max_checks, int64_t* n_checks) {
+  int rc = PSG_OK;
+  if (!p || p->steps < 0) return fail(PSG_ERR_CONFIG, "bad run parameters");
+  psg_slab* s0 = sl[0];
+  const int64_t rec = 3 * s0->n + 2;
+  int64_t want = 0;
+  if (p->measure_every > 0) want = p->steps / p->measure_every + 1;
+  want = std::min(want, max_checks);
+  for (psg_slab* s : sl) {
+    CU_TRY(cudaSetDevice(s->device));
+    rc = ensure_hist(s, want);
+    if (rc) return rc;
+  }
+  int64_t nc = 0;
+  std::vector<double> steps_of;
+  auto plain = [&](int64_t t) {  // step t is a bare update (no measure / norm / re-impose)
+    const int64_t sidx = p->step_offset + t;
+    const bool meas = p->measure_every > 0 && sidx - 1 > 0 && (sidx - 1) % p->measure_every == 0;
+    const bool norm = p->norm_every > 0 && sidx % p->norm_every == 0;
+    const bool reimp = p->reimpose_every > 0 && p->n_impose > 0 && sidx % p->reimpose_every == 0;
+    return !meas && !norm && !reimp;
+  };
+  // two-sweep passes: a whole-lattice slab, or slabs of W >= 2 (two halo
+  // planes per face); the march only for a whole lattice
+  bool t2_ok = true;
+  for (psg_slab* s : sl)
+    t2_ok = t2_ok && s->use_t2 && !s->use_ac && (!tr || s->w >= 2) && s->field_elems < (1ull << 32);
+  const bool whole = !tr;
+  auto set_all = [&](auto&& f) {
+    for (psg_slab* s : sl) {
+      CU_TRY(cudaSetDevice(s->device));
+      const int r = f(s);
+      if (r) return r;
+    }
+    return (int)PSG_OK;
+  };
+  if (tr) tr->deep = false;
+  for (int64_t t = 1; t <= p->steps; ++t) {
+    if (((whole && s0->use_march) || t2_ok) && s0->pending == s0->scal + S_ONE && plain(t)) {
+      int64_t run = 1;
+      while (t + run <= p->steps && plain(t + run)) ++run;
+      if ((!s0->use_march || tr) && run >= 2) {
+        // pairs of plain steps: two sweeps per pass over HBM
+        const int64_t pairs = run / 2;
+        for (int64_t q = 0; q < pairs; ++q) {
+          rc = tr ? multi_sweep2(sl, tr) : do_sweep2(s0);
+          if (rc) return rc;
+        }
+        t += 2 * pairs - 1;
+        continue;
+      }
+      // the step after a run carries the measure / norm / impose: include it only if plain
+      if (whole && run >= 2) {
+        while (run > 0) {
+          const int chunk = (int)std::min<int64_t>(run, 1 << 20);
+          rc = do_march(s0, chunk);
+          if (rc) return rc;
+          run -= chunk;
+          t += chunk;
+        }
+        --t;
+        continue;
+      }
+    }
+    const int64_t sidx = p->step_offset + t;   // global sweep number
+    const int64_t state_idx = sidx - 1;
+    unsigned flags = PSG_F_WRITE;
+    const bool meas = p->measure_every > 0 && state_idx > 0 && state_idx % p->measure_every == 0 &&
+                      nc < want;
+    const bool norm = p->norm_every > 0 && sidx % p->norm_every == 0;
+    if (meas) flags |= PSG_F_MEASURE;
+    if (norm) flags |= PSG_F_NORM;
+    rc = tr ? multi_sweep(sl, tr, flags, true) : do_sweep(s0, 1, s0->w, flags, true);
+    if (rc) return rc;
+    const unsigned q = qmask_of(flags);
+    if (q) {
+      if (tr) {
+        // zero-padded global plane-sum vectors: one non-zero contributor per
+        // slot, so the sum is exact and the combine M-invariant
+        rc = set_all([&](psg_slab* s) {
+          CU_TRY(cudaMemsetAsync(s->plane_sums, 0, (size_t)NQ * s->n * sizeof(double), s->stream));
+          return do_reduce(s, 1, s->w, q, false, nullptr);
+        });
+        if (rc) return rc;
+        rc = tr->allreduce();
+        if (rc) return rc;
+        rc = set_all([&](psg_slab* s) { return do_combine(s, q, meas ? s->hist_dev + nc * rec : nullptr); });
+      } else {
+        rc = do_reduce(s0, 1, s0->n, q, true, meas ? s0->hist_dev + nc * rec : nullptr);
+      }
+      if (rc) return rc;
+      if (meas) {
+        steps_of.push_back((double)state_idx);
+        ++nc;
+      }
+    }
+    for (psg_slab* s : sl) {
+      s->cur = 1 - s->cur;
+      s->pending = norm ? s->scal + S_FACTOR : s->scal + S_ONE;
+    }
+    if (p->reimpose_every > 0 && sidx % p->reimpose_every == 0) {
+      for (int k = 0; k < p->n_impose && k < 3; ++k) {
+        rc = set_all([&](psg_slab* s) { return psg_impose(s, p->impose_axis[k], p->impose_sign[k], 0); });
+        if (rc) return rc;
+      }
+      if (tr) tr->deep = false;
+    }
+  }
+  CU_TRY(cudaSetDevice(s0->device));
+  if (hist && nc > 0) {
+    CU_TRY(cudaMemcpyAsync(hist, s0->hist_dev, (size_t)nc * rec * sizeof(double),
+                           cudaMemcpyDeviceToHost, s0->stream));
+  }
+  rc = set_all([&](psg_slab* s) {
+    CU_TRY(cudaStreamSynchronize(s->stream));
+    return (int)PSG_OK;
+  });
+  if (rc) return rc;
+  if (hist)
+    for (int64_t k = 0; k < nc; ++k) hist[k * rec] = steps_of[k];
+  if (n_checks) *n_checks = nc;
+  return PSG_OK;
+}

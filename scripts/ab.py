@@ -24,7 +24,9 @@ def build(name, flags):
     out = os.path.join(ABDIR, f"libpsigpu_{name}.so")
     cmd = ["/usr/local/cuda/bin/nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3",
            "-lineinfo", "--fmad=false", "-std=c++17", *flags, "-Xcompiler", "-fPIC", "-shared",
-           "-cudart", "static", "-I", os.path.join(ROOT, "include"), "-o", out, src]
+           "-cudart", "static", "-I", os.path.join(ROOT, "include"),
+           # a --src= copy finds its own headers first, then the tree's
+           "-I", os.path.join(ROOT, "paper_0904_0939_b200", "csrc"), "-o", out, src]
     subprocess.run(cmd, check=True)
     print(out)
 
