@@ -187,8 +187,11 @@ int psg_get_field(psg_slab* s, double* host, int64_t first, int64_t count);
  * psg_fill_potential: V on the slab's planes, kind 0 harmonic (0.5 r) r,
  * 1 Coulomb -1/max(r, a/2), 2 Cornell -alpha/max(r,a/2) + sigma max(r,a/2)
  * (params alpha, sigma), 3 harmonic plus 8 Gaussian wells (params: centres
- * [8][3] by storage axis, depths[8], widths[8]); r from the lattice centre as
- * in workloads.py (bitwise, except the wells' exp: <= 1 ulp per term), then
+ * [8][3] by storage axis, depths[8], widths[8]), 4 psibox coulomb (0 for
+ * r < a, -1/r + 1/a beyond; potential.py:126-136), 5 psibox dodecahedron
+ * (params: face normals[12][3], limit, depth; potential.py:165-183); r from
+ * the lattice centre as in workloads.py / potential.py (bitwise, except the
+ * wells' exp: <= 1 ulp per term), then
  * the same checks as psg_set_potential. */
 int psg_fill_uniform(psg_slab* s, uint64_t seed);
 /* Download potential planes (dense, like psg_get_field). */

@@ -59,12 +59,14 @@ __global__ void k_fill_uniform(double* __restrict__ psi, uint64_t k0, uint64_t k
   }
 }
 
-constexpr int POT_HARMONIC = 0, POT_COULOMB = 1, POT_CORNELL = 2, POT_WELLS = 3;
+constexpr int POT_HARMONIC = 0, POT_COULOMB = 1, POT_CORNELL = 2, POT_WELLS = 3,
+              POT_COULOMB_SHIFTED = 4, POT_DODECAHEDRON = 5;
 struct PotParams {
-  double p[48];   // cornell: alpha, sigma; wells: centres[8][3], depths[8], widths[8]
+  double p[48];   // cornell: alpha, sigma; wells: centres[8][3], depths[8], widths[8];
+                  // dodecahedron: normals[12][3], limit, depth
 };
 
-// V on every local plane (padding zero), the workloads.py expressions:
+// V on every local plane (padding zero), the workloads.py / potential.py expressions:
 // off = (i - center) a, r = sqrt((dx^2 + dy^2) + dz^2)
 __global__ void k_fill_potential(double* __restrict__ v, int kind, const PotParams prm, int n,
                                  int pitch, long long plane_stride, int planes, int x_off,
@@ -90,6 +92,24 @@ __global__ void k_fill_potential(double* __restrict__ v, int kind, const PotPara
         val = __dmul_rn(__dmul_rn(0.5, r), r);
       } else if (kind == POT_COULOMB) {
         val = __ddiv_rn(-1.0, fmax(r, half_a));
+      } else if (kind == POT_COULOMB_SHIFTED) {
+        // potential.py:126-136: 0 for r < a, -1/r + 1/a beyond
+        val = r >= a ? __dadd_rn(__ddiv_rn(-1.0, r), __ddiv_rn(1.0, a)) : 0.0;
+      } else if (kind == POT_DODECAHEDRON) {
+        // potential.py:165-183: u = (2i - n - 1)/(n - 1) per axis; inside iff every face
+        // normal's (nx ux + ny uy) + nz uz <= limit
+        const double dn = (double)n, dm = __dsub_rn(dn, 1.0);
+        const double ux = __ddiv_rn(__dsub_rn(__dsub_rn(__dmul_rn(2.0, (double)gi), dn), 1.0), dm);
+        const double uy = __ddiv_rn(__dsub_rn(__dsub_rn(__dmul_rn(2.0, (double)j), dn), 1.0), dm);
+        const double uz = __ddiv_rn(__dsub_rn(__dsub_rn(__dmul_rn(2.0, (double)k), dn), 1.0), dm);
+        bool inside = true;
+        for (int f = 0; f < 12; ++f) {
+          const double dot = __dadd_rn(__dadd_rn(__dmul_rn(prm.p[3 * f], ux),
+                                                 __dmul_rn(prm.p[3 * f + 1], uy)),
+                                       __dmul_rn(prm.p[3 * f + 2], uz));
+          inside = inside && dot <= prm.p[36];
+        }
+        val = inside ? prm.p[37] : 0.0;
       } else if (kind == POT_CORNELL) {
         const double rf = fmax(r, half_a);
         val = __dadd_rn(__ddiv_rn(-prm.p[0], rf), __dmul_rn(prm.p[1], rf));

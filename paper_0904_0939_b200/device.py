@@ -237,7 +237,9 @@ class Slab:
 
     def fill_potential(self, kind: int, params=()):
         """V generated on the device: kind 0 harmonic, 1 Coulomb (floored),
-        2 Cornell (alpha, sigma), 3 harmonic + 8 wells (centres, depths, widths)."""
+        2 Cornell (alpha, sigma), 3 harmonic + 8 wells (centres, depths, widths),
+        4 psibox coulomb, 5 psibox dodecahedron (normals, limit, depth) -- see
+        potential.device_generator for the named psibox potentials."""
         prm = np.ascontiguousarray(np.asarray(params, dtype=np.float64).ravel())
         bad = np.zeros(3, dtype=np.int64)
         rc = self._lib.psg_fill_potential(self._h, int(kind), dptr(prm) if prm.size else None,

@@ -35,6 +35,7 @@ __all__ = [
     "save_potential",
     "precompute_coefficients",
     "coefficients",
+    "device_generator",
 ]
 
 GOLDEN_RATIO = 0.5 * (1.0 + np.sqrt(5.0))
@@ -191,6 +192,24 @@ def dodecahedron(spec: LatticeSpec, depth: float = -100.0) -> PotentialGrid:
         inside &= (nx * ux + ny * uy + nz * uz) <= limit
     v = np.where(inside, float(depth), 0.0)
     return _build(spec, v, v_inf=0.0, unbounded=False, name="dodecahedron")
+
+
+# kinds of psg_fill_potential (include/psigpu.h) for the named potentials
+_DEVICE_KINDS = {"harmonic": 0, "coulomb": 4, "dodecahedron": 5}
+
+
+def device_generator(name: str, depth: float = -100.0):
+    """(kind, params) for Slab.fill_potential: the named potential generated on
+    the device, bitwise equal to ``harmonic(spec).v`` / ``coulomb(spec).v`` /
+    ``dodecahedron(spec, depth).v`` (no host array; what a 2048^3 lattice needs).
+    v_inf / unbounded stay those of the host constructors."""
+    if name not in _DEVICE_KINDS:
+        raise ConfigError(f"no device generator for potential {name!r}")
+    if name == "dodecahedron":
+        normals = np.asarray(_DODEC_NORMALS, dtype=np.float64).ravel()
+        return _DEVICE_KINDS[name], np.concatenate(
+            [normals, [_DODEC_OFFSET + _DODEC_BOUNDARY_SLACK, float(depth)]])
+    return _DEVICE_KINDS[name], ()
 
 
 def save_potential(grid: PotentialGrid, path) -> None:

@@ -365,6 +365,23 @@ class TestStates:
 
 # ---------------------------------------------------------------- reference fixtures
 class TestGolden:
+    def test_device_potentials_match_reference_fixtures(self, gpu_lib):
+        """psg_fill_potential's psibox generators against the reference's own
+        harmonic / coulomb / dodecahedron grids (tests/golden/potentials.npz)."""
+        from paper_0904_0939_b200.device import Slab
+        from paper_0904_0939_b200.potential import device_generator
+
+        g = gold("potentials")
+        cases = [((8, 0.3), "harmonic", "harmonic8", -100.0), ((8, 0.3), "coulomb", "coulomb8", -100.0),
+                 ((9, 0.5), "coulomb", "coulomb9", -100.0), ((9, 0.5), "harmonic", "harmonic9", -100.0),
+                 ((12, 0.1), "dodecahedron", "dodec12", -100.0),
+                 ((12, 0.1), "dodecahedron", "dodec12_d7", -7.0)]
+        for (n, a), name, key, depth in cases:
+            spec = LatticeSpec(N=n, a=a, m=1.0, dtau=a * a / 4)
+            with Slab(spec) as s:
+                s.fill_potential(*device_generator(name, depth=depth))
+                assert np.array_equal(s.get_potential(), g[key]), key
+
     @pytest.mark.parametrize("n", [4, 5, 8, 13])
     def test_kernels_api(self, gpu_lib, n):
         g = gold("kernels")

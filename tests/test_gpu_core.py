@@ -312,3 +312,10 @@ def test_device_inputs_match_host_recipes(gpu_lib, n, w, x_lo):
                 np.testing.assert_allclose(dev, host, rtol=1e-14, atol=1e-14)
             else:
                 assert np.array_equal(dev, host), name
+        # the psibox constructors (potential.py:126-183), bitwise
+        from paper_0904_0939_b200 import potential as pot
+        for name, grid in (("harmonic", pot.harmonic(spec)), ("coulomb", pot.coulomb(spec)),
+                           ("dodecahedron", pot.dodecahedron(spec, depth=-7.5))):
+            kind, params = pot.device_generator(name, depth=-7.5)
+            s.fill_potential(kind, params)
+            assert np.array_equal(s.get_potential(), grid.v[x_lo - 1:x_lo + ww + 1]), name

@@ -119,6 +119,19 @@ def test_potentials_match_reference():
     assert np.array_equal(hand.coef_c, g["hand_c"])
 
 
+def test_device_generator_parameters():
+    from paper_0904_0939_b200.errors import ConfigError
+    from paper_0904_0939_b200.potential import device_generator
+
+    assert device_generator("harmonic") == (0, ())
+    assert device_generator("coulomb") == (4, ())
+    kind, prm = device_generator("dodecahedron", depth=-3.0)
+    assert kind == 5 and prm.shape == (38,) and prm[-1] == -3.0
+    assert prm[36] == 0.5 * (1.0 + np.sqrt(5.0)) + 1e-12
+    with pytest.raises(ConfigError):
+        device_generator("custom")
+
+
 def test_coefficients_match_reference_kernels_fixture():
     g = gold("kernels")
     for n in (4, 5, 8, 13):
