@@ -236,6 +236,9 @@ def _pinned(shape):
     return torch.empty(shape, dtype=torch.float64, pin_memory=True).numpy()
 
 
+E2E_WARMUP = 2
+
+
 def run_single(args):
     import torch
 
@@ -335,11 +338,16 @@ def run_single(args):
     grid = PotentialGrid(spec=spec, v=vhost, v_inf=0.0, unbounded=False, name="custom")
     init = Field3D(spec, psi0)
     e2e_times = []
-    for _ in range(5):   # the user-facing call, from host arrays, median of five
+    # the user-facing call, from host arrays: two untimed warm-up calls (the
+    # memory pool and the pinned result cache reach steady state: a caller
+    # still holding the previous result makes the second call allocate one
+    # more pinned block), then the median of five
+    for i in range(E2E_WARMUP + 5):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         state = evolve_fixed(init, grid, args.steps, m, norm_every=m)
-        e2e_times.append(time.perf_counter() - t0)
+        if i >= E2E_WARMUP:
+            e2e_times.append(time.perf_counter() - t0)
     t_e2e = statistics.median(e2e_times)
     e2e = n ** 3 * args.steps / t_e2e / 1e9
     h2d = 2 * ext ** 3 * 8
@@ -374,7 +382,8 @@ def run_single(args):
                 "d2h_bytes_per_step": d2h / args.steps,
                 "api": "paper_0904_0939_b200.evolve_fixed(Field3D, PotentialGrid) from pinned "
                        "host memory, psi0+V uploaded and psi downloaded inside the timed region",
-                "calls_s": [round(t, 4) for t in e2e_times], "statistic": "median of 5 calls"},
+                "calls_s": [round(t, 4) for t in e2e_times],
+                "statistic": f"median of 5 calls after {E2E_WARMUP} untimed warm-up calls"},
         "gpu_launches": launches,
         "cpu_baseline": cpu,
         "observables": {"E_last": float(np.sum(sums[-1][0]) / np.sum(sums[-1][1]))
@@ -494,7 +503,7 @@ def run_dist(args):
         psi0[1:-1] = workloads.uniform_start(spec)
         init = Field3D(spec, psi0)
     e2e_times = []
-    for _ in range(3):
+    for i in range(E2E_WARMUP + 3):
         dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -503,7 +512,8 @@ def run_dist(args):
                                max_snapshots=0, norm_every=m, fixed=True)
         dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
         dist.all_reduce(dt, op=dist.ReduceOp.MAX)
-        e2e_times.append(float(dt.item()))
+        if i >= E2E_WARMUP:
+            e2e_times.append(float(dt.item()))
     t_e2e = statistics.median(e2e_times)
     if rank == 0:
         line = {
@@ -535,7 +545,8 @@ def run_dist(args):
                            "scatter_initial=True, fixed=True) from host arrays on rank 0 (psi0) "
                            "and every rank (V); psi gathered to rank 0 inside the timed region",
                     "calls_s": [round(t, 4) for t in e2e_times],
-                    "statistic": "median of 3 calls, max over ranks"},
+                    "statistic": f"median of 3 calls after {E2E_WARMUP} untimed warm-up "
+                                 "calls, max over ranks"},
             "gpu_launches": int(launches.item()),
             "cpu_baseline": None,
         }

@@ -44,6 +44,20 @@ __device__ __forceinline__ bool mbar_try_u(uint32_t bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// non-blocking probe (test_wait): issued well before its result is needed,
+// so the ~150-cycle barrier latency overlaps other work instead of sitting
+// between the wait and the shared loads it guards
+__device__ __forceinline__ bool mbar_test_u(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
 // the retry loop (with the watchdog) out of line: the hot path is one
 // try_wait and a branch
 __device__ __noinline__ void mbar_wait_slow(uint32_t bar, uint32_t parity) {
@@ -140,6 +154,21 @@ __device__ __forceinline__ bool t2b_interior(const T2Item& I, int n, int x_off) 
   return (I.j >= 2) & (I.j + TB <= n) & (I.k >= 2) & (I.k + TX <= n) & (x_off + I.z0 >= 2) &
          (x_off + I.z1 < n);
 }
+// per warp role: E row j = I.j - 1 + w (columns k0 .. k0+63) and the ring
+// columns k0-1, k0+64 of rows j0 .. j0+TB-1.  Tile rows never leave the
+// lattice when N is a multiple of TB (nor columns when it is one of 64), so
+// the tile-row warps run masked only on the first and last z-chunks.
+__device__ __forceinline__ bool t2b_z_interior(const T2Item& I, int n, int x_off) {
+  return (x_off + I.z0 >= 2) & (x_off + I.z1 < n);
+}
+__device__ __forceinline__ bool t2b_row_interior(const T2Item& I, int w, int n, int x_off) {
+  const int j = I.j - 1 + w;
+  return (j >= 1) & (j <= n) & (I.k + TX - 1 <= n) & t2b_z_interior(I, n, x_off);
+}
+template <int TB>
+__device__ __forceinline__ bool t2b_ring_interior(const T2Item& I, int n, int x_off) {
+  return (I.k >= 2) & (I.k + TX <= n) & (I.j + TB - 1 <= n) & t2b_z_interior(I, n, x_off);
+}
 
 
 // one work item of an E-row warp (MASK: item touches the lattice boundary)
@@ -177,6 +206,9 @@ __device__ __forceinline__ void t2b_rows_item(const SweepArgs& args, const T2Ite
   double2 c_b = lds2_u(base + nx.slot * G::STAGE);
   int cur = nx.slot;
   nx.next();
+#if !defined(PSG_NO_PROBE)
+  bool okf = mbar_test_u(fb + nx.slot * 8, nx.ph);   // stage of the first loop plane
+#endif
   double2 c_c;
   double2 q0 = make_double2(0.0, 0.0), q1 = q0, q2 = q0;
   double2 a0 = q0, a1 = q0, a2 = q0, f0 = q0, f1 = q0, f2 = q0;
@@ -185,7 +217,16 @@ __device__ __forceinline__ void t2b_rows_item(const SweepArgs& args, const T2Ite
   auto plane = [&](const double2& cp, const double2& cc, double2& cn, double2& qw,
                    const double2& qm, const double2& qmm, double2& aw, double2& fw,
                    const double2& am, const double2& fm) {
+#if defined(PSG_NO_PROBE)
     mbar_wait_u(fb + nx.slot * 8, nx.ph);
+#else
+    if (!okf) mbar_wait_slow(fb + nx.slot * 8, nx.ph);   // probed one plane earlier
+    // all warps' psi' of plane g-1, needed by step 2 below: probe now (ahead
+    // of the shared loads, which the compiler keeps in order)
+    const uint32_t gp = g - 1;
+    const uint32_t rbar = fb + (2 * S + (gp & 3u)) * 8, rph = (gp >> 2) & 1u;
+    const bool okr = g == 0 || mbar_test_u(rbar, rph);
+#endif
     cn = lds2_u(base + nx.slot * G::STAGE);
     const uint32_t sc = base + cur * G::STAGE;
     const double2 jm = lds2_u(sc - BOXW * 8);
@@ -208,9 +249,16 @@ __device__ __forceinline__ void t2b_rows_item(const SweepArgs& args, const T2Ite
     mbar_arrive_u(fb + (2 * S + (g & 3u)) * 8);
     cur = nx.slot;
     nx.next();
+#if !defined(PSG_NO_PROBE)
+    okf = mbar_test_u(fb + nx.slot * 8, nx.ph);   // the next plane's stage
+#endif
     if (g > 0) {
+#if defined(PSG_NO_PROBE)
       const uint32_t gp = g - 1;
       mbar_wait_u(fb + (2 * S + (gp & 3u)) * 8, (gp >> 2) & 1u);
+#else
+      if (!okr) mbar_wait_slow(rbar, rph);
+#endif
       if (STEP2) {
         const uint32_t rq = base + ROFF + rr;
         const double2 rjm = lds2_u(rq - BOXW * 8);
@@ -262,7 +310,11 @@ __device__ __forceinline__ void t2b_rows(const SweepArgs& args, uint32_t sm0, in
   uint32_t g = 0;   // ring plane counter (runs across items)
   for (int item = blockIdx.x; item < args.nitems; item += gridDim.x) {
     const T2Item I = t2b_item<TB>(args, item);
+#if defined(PSG_TILE_MASK)
     if (t2b_interior<TB>(I, args.n, args.x_off))
+#else
+    if (t2b_row_interior(I, w, args.n, args.x_off))
+#endif
       t2b_rows_item<S, TB, STEP2, FASTC, false>(args, I, fb, base, w, lane, nx, g);
     else
       t2b_rows_item<S, TB, STEP2, FASTC, true>(args, I, fb, base, w, lane, nx, g);
@@ -290,11 +342,21 @@ __device__ __forceinline__ void t2b_ring_item(const SweepArgs& args, const T2Ite
   double c_b = lds1_u(base + nx.slot * G::STAGE);
   int cur = nx.slot;
   nx.next();
+#if !defined(PSG_NO_PROBE)
+  bool okf = mbar_test_u(fb + nx.slot * 8, nx.ph);
+#endif
   double c_c;
   const int pend = I.z1 + 2;
   int p = I.z0 - 1;
   auto plane = [&](const double& cp, const double& cc, double& cn) {
+#if defined(PSG_NO_PROBE)
     mbar_wait_u(fb + nx.slot * 8, nx.ph);
+#else
+    if (!okf) mbar_wait_slow(fb + nx.slot * 8, nx.ph);
+    const uint32_t gp = g - 1;
+    const uint32_t rbar = fb + (2 * S + (gp & 3u)) * 8, rph = (gp >> 2) & 1u;
+    const bool okr = g == 0 || mbar_test_u(rbar, rph);
+#endif
     cn = lds1_u(base + nx.slot * G::STAGE);
     const uint32_t sc = base + cur * G::STAGE;
     const double jm = lds1_u(sc - BOXW * 8);
@@ -315,7 +377,12 @@ __device__ __forceinline__ void t2b_ring_item(const SweepArgs& args, const T2Ite
     mbar_arrive_u(fb + (2 * S + (g & 3u)) * 8);
     cur = nx.slot;
     nx.next();
+#if defined(PSG_NO_PROBE)
     if (g > 0) mbar_wait_u(fb + (2 * S + ((g - 1) & 3u)) * 8, ((g - 1) >> 2) & 1u);
+#else
+    okf = mbar_test_u(fb + nx.slot * 8, nx.ph);
+    if (!okr) mbar_wait_slow(rbar, rph);
+#endif
     ++p;
     ++g;
   };
@@ -342,7 +409,11 @@ __device__ __forceinline__ void t2b_ringw(const SweepArgs& args, uint32_t sm0, i
   uint32_t g = 0;
   for (int item = blockIdx.x; item < args.nitems; item += gridDim.x) {
     const T2Item I = t2b_item<TB>(args, item);
+#if defined(PSG_TILE_MASK)
     if (t2b_interior<TB>(I, args.n, args.x_off))
+#else
+    if (t2b_ring_interior<TB>(I, args.n, args.x_off))
+#endif
       t2b_ring_item<S, TB, FASTC, false>(args, I, fb, base, rrow, rcol, active, lane, nx, g);
     else
       t2b_ring_item<S, TB, FASTC, true>(args, I, fb, base, rrow, rcol, active, lane, nx, g);
