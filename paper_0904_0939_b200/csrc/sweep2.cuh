@@ -58,6 +58,27 @@ __device__ __forceinline__ bool mbar_test_u(uint32_t bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// wait for a phase unless a probe already saw it complete: one asm block
+// (the retry loop and its watchdog inside), so the compiler emits no
+// reconvergence region or call around it
+__device__ __forceinline__ void mbar_wait_if(bool done, uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1, P2;\n\t.reg .u32 C;\n\t"
+      "setp.ne.u32 P1, %0, 0;\n\t"
+      "@P1 bra DONE;\n\t"
+      "mov.u32 C, 0;\n"
+      "WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P2, [%1], %2;\n\t"
+      "@P2 bra DONE;\n\t"
+      "add.u32 C, C, 1;\n\t"
+      "setp.gt.u32 P1, C, 16777216;\n\t"
+      "@P1 trap;\n\t"
+      "bra WAIT;\n"
+      "DONE:\n}"
+      :
+      : "r"((uint32_t)done), "r"(bar), "r"(parity)
+      : "memory");
+}
 // the retry loop (with the watchdog) out of line: the hot path is one
 // try_wait and a branch
 __device__ __noinline__ void mbar_wait_slow(uint32_t bar, uint32_t parity) {
@@ -206,9 +227,7 @@ __device__ __forceinline__ void t2b_rows_item(const SweepArgs& args, const T2Ite
   double2 c_b = lds2_u(base + nx.slot * G::STAGE);
   int cur = nx.slot;
   nx.next();
-#if !defined(PSG_NO_PROBE)
   bool okf = mbar_test_u(fb + nx.slot * 8, nx.ph);   // stage of the first loop plane
-#endif
   double2 c_c;
   double2 q0 = make_double2(0.0, 0.0), q1 = q0, q2 = q0;
   double2 a0 = q0, a1 = q0, a2 = q0, f0 = q0, f1 = q0, f2 = q0;
@@ -217,16 +236,12 @@ __device__ __forceinline__ void t2b_rows_item(const SweepArgs& args, const T2Ite
   auto plane = [&](const double2& cp, const double2& cc, double2& cn, double2& qw,
                    const double2& qm, const double2& qmm, double2& aw, double2& fw,
                    const double2& am, const double2& fm) {
-#if defined(PSG_NO_PROBE)
-    mbar_wait_u(fb + nx.slot * 8, nx.ph);
-#else
-    if (!okf) mbar_wait_slow(fb + nx.slot * 8, nx.ph);   // probed one plane earlier
+    mbar_wait_if(okf, fb + nx.slot * 8, nx.ph);   // probed one plane earlier
     // all warps' psi' of plane g-1, needed by step 2 below: probe now (ahead
     // of the shared loads, which the compiler keeps in order)
     const uint32_t gp = g - 1;
     const uint32_t rbar = fb + (2 * S + (gp & 3u)) * 8, rph = (gp >> 2) & 1u;
-    const bool okr = g == 0 || mbar_test_u(rbar, rph);
-#endif
+    const bool okr = mbar_test_u(rbar, rph);
     cn = lds2_u(base + nx.slot * G::STAGE);
     const uint32_t sc = base + cur * G::STAGE;
     const double2 jm = lds2_u(sc - BOXW * 8);
@@ -249,31 +264,24 @@ __device__ __forceinline__ void t2b_rows_item(const SweepArgs& args, const T2Ite
     mbar_arrive_u(fb + (2 * S + (g & 3u)) * 8);
     cur = nx.slot;
     nx.next();
-#if !defined(PSG_NO_PROBE)
     okf = mbar_test_u(fb + nx.slot * 8, nx.ph);   // the next plane's stage
-#endif
-    if (g > 0) {
-#if defined(PSG_NO_PROBE)
-      const uint32_t gp = g - 1;
-      mbar_wait_u(fb + (2 * S + (gp & 3u)) * 8, (gp >> 2) & 1u);
-#else
-      if (!okr) mbar_wait_slow(rbar, rph);
-#endif
-      if (STEP2) {
-        const uint32_t rq = base + ROFF + rr;
-        const double2 rjm = lds2_u(rq - BOXW * 8);
-        const double2 rjp = lds2_u(rq + BOXW * 8);
-        const double rkm = lds1_u(rq - 8);
-        const double rkp = lds1_u(rq + 16);
-        const double o0 = upd(am.x, fm.x, qm.x, qmm.x, qw.x, rjm.x, rjp.x, rkm, qm.y);
-        const double o1 = upd(am.y, fm.y, qm.y, qmm.y, qw.y, rjm.y, rjp.y, qm.x, rkp);
-        if (p > I.z0) {   // plane p-1 >= z0
-          double* dst = args.out + doff;
-          if (!MASK || ok1) {
-            *reinterpret_cast<double2*>(dst) = make_double2(o0, o1);
-          } else if (ok0) {
-            *dst = o0;
-          }
+    // (the kernel's first plane reads a pre-completed phase: its step 2 is
+    // discarded like every item's first two)
+    mbar_wait_if(okr, rbar, rph);
+    if (STEP2) {
+      const uint32_t rq = base + ROFF + rr;
+      const double2 rjm = lds2_u(rq - BOXW * 8);
+      const double2 rjp = lds2_u(rq + BOXW * 8);
+      const double rkm = lds1_u(rq - 8);
+      const double rkp = lds1_u(rq + 16);
+      const double o0 = upd(am.x, fm.x, qm.x, qmm.x, qw.x, rjm.x, rjp.x, rkm, qm.y);
+      const double o1 = upd(am.y, fm.y, qm.y, qmm.y, qw.y, rjm.y, rjp.y, qm.x, rkp);
+      if (p > I.z0) {   // plane p-1 >= z0
+        double* dst = args.out + doff;
+        if (!MASK || ok1) {
+          *reinterpret_cast<double2*>(dst) = make_double2(o0, o1);
+        } else if (ok0) {
+          *dst = o0;
         }
       }
     }
@@ -307,7 +315,7 @@ __device__ __forceinline__ void t2b_rows(const SweepArgs& args, uint32_t sm0, in
   const uint32_t fb = sm0 + C::BAR_OFF;               // full[S], empty[S], rfull[4]
   const uint32_t base = sm0 + (uint32_t)(((w + 1) * BOXW + 2 * lane + 2) * 8);
   StageCursor<S> nx;
-  uint32_t g = 0;   // ring plane counter (runs across items)
+  uint32_t g = 4;   // ring plane counter (runs across items; 0..3 are the pre-completed phases)
   for (int item = blockIdx.x; item < args.nitems; item += gridDim.x) {
     const T2Item I = t2b_item<TB>(args, item);
 #if defined(PSG_TILE_MASK)
@@ -342,21 +350,15 @@ __device__ __forceinline__ void t2b_ring_item(const SweepArgs& args, const T2Ite
   double c_b = lds1_u(base + nx.slot * G::STAGE);
   int cur = nx.slot;
   nx.next();
-#if !defined(PSG_NO_PROBE)
   bool okf = mbar_test_u(fb + nx.slot * 8, nx.ph);
-#endif
   double c_c;
   const int pend = I.z1 + 2;
   int p = I.z0 - 1;
   auto plane = [&](const double& cp, const double& cc, double& cn) {
-#if defined(PSG_NO_PROBE)
-    mbar_wait_u(fb + nx.slot * 8, nx.ph);
-#else
-    if (!okf) mbar_wait_slow(fb + nx.slot * 8, nx.ph);
+    mbar_wait_if(okf, fb + nx.slot * 8, nx.ph);
     const uint32_t gp = g - 1;
     const uint32_t rbar = fb + (2 * S + (gp & 3u)) * 8, rph = (gp >> 2) & 1u;
-    const bool okr = g == 0 || mbar_test_u(rbar, rph);
-#endif
+    const bool okr = mbar_test_u(rbar, rph);
     cn = lds1_u(base + nx.slot * G::STAGE);
     const uint32_t sc = base + cur * G::STAGE;
     const double jm = lds1_u(sc - BOXW * 8);
@@ -377,12 +379,8 @@ __device__ __forceinline__ void t2b_ring_item(const SweepArgs& args, const T2Ite
     mbar_arrive_u(fb + (2 * S + (g & 3u)) * 8);
     cur = nx.slot;
     nx.next();
-#if defined(PSG_NO_PROBE)
-    if (g > 0) mbar_wait_u(fb + (2 * S + ((g - 1) & 3u)) * 8, ((g - 1) >> 2) & 1u);
-#else
     okf = mbar_test_u(fb + nx.slot * 8, nx.ph);
-    if (!okr) mbar_wait_slow(rbar, rph);
-#endif
+    mbar_wait_if(okr, rbar, rph);
     ++p;
     ++g;
   };
@@ -406,7 +404,7 @@ __device__ __forceinline__ void t2b_ringw(const SweepArgs& args, uint32_t sm0, i
   const bool active = lane < 2 * TB;
   const uint32_t base = sm0 + (uint32_t)(((rrow + 1) * BOXW + rcol) * 8);
   StageCursor<S> nx;
-  uint32_t g = 0;
+  uint32_t g = 4;
   for (int item = blockIdx.x; item < args.nitems; item += gridDim.x) {
     const T2Item I = t2b_item<TB>(args, item);
 #if defined(PSG_TILE_MASK)
@@ -443,6 +441,11 @@ __global__ void __launch_bounds__(T2BGeo<TB>::THREADS, T2BGeo<TB>::MINB)
     fence_barrier_init();
   }
   __syncthreads();
+  // ring planes count from 4: every consumer lane completes phase 0 of each
+  // slot once, so the first planes' waits need no g > 0 test
+  if (warp < G::CW) {
+    for (int r = 0; r < RS; ++r) mbar_arrive(&rfull[r]);
+  }
   pdl_launch_dependents();
   pdl_wait();
   if (warp == G::CW) {
