@@ -265,10 +265,10 @@ __device__ __forceinline__ void t2b_rows_item(const SweepArgs& args, const T2Ite
     cur = nx.slot;
     nx.next();
     okf = mbar_test_u(fb + nx.slot * 8, nx.ph);   // the next plane's stage
-    // (the kernel's first plane reads a pre-completed phase: its step 2 is
-    // discarded like every item's first two)
+    // (the kernel's first plane waits on a pre-completed phase; no item
+    // stores or computes step 2 in its first two planes)
     mbar_wait_if(okr, rbar, rph);
-    if (STEP2) {
+    if (STEP2 && p > I.z0) {   // plane p-1 >= z0: an output plane of this item
       const uint32_t rq = base + ROFF + rr;
       const double2 rjm = lds2_u(rq - BOXW * 8);
       const double2 rjp = lds2_u(rq + BOXW * 8);
@@ -276,13 +276,11 @@ __device__ __forceinline__ void t2b_rows_item(const SweepArgs& args, const T2Ite
       const double rkp = lds1_u(rq + 16);
       const double o0 = upd(am.x, fm.x, qm.x, qmm.x, qw.x, rjm.x, rjp.x, rkm, qm.y);
       const double o1 = upd(am.y, fm.y, qm.y, qmm.y, qw.y, rjm.y, rjp.y, qm.x, rkp);
-      if (p > I.z0) {   // plane p-1 >= z0
-        double* dst = args.out + doff;
-        if (!MASK || ok1) {
-          *reinterpret_cast<double2*>(dst) = make_double2(o0, o1);
-        } else if (ok0) {
-          *dst = o0;
-        }
+      double* dst = args.out + doff;
+      if (!MASK || ok1) {
+        *reinterpret_cast<double2*>(dst) = make_double2(o0, o1);
+      } else if (ok0) {
+        *dst = o0;
       }
     }
     if (STEP2) doff += pstride;
