@@ -364,7 +364,10 @@ int psg_tune(psg_slab* s, int blocks_per_sm, int zchunk, int stages);
  * alternate the z-march direction every sweep so a sweep starts on the planes
  * its predecessor wrote last, still in L2 (default 1; bitwise unchanged),
  * 3 = tile rows of the two-sweep pass, 8 (two blocks per SM) or 16 (one
- * block per SM, default; bitwise unchanged). */
+ * block per SM, default; bitwise unchanged), 4 = always take the range-checked
+ * coefficient path, 5 = TMA stages of the 16-row two-sweep pass (6 or 9),
+ * 6 = two-sweep passes alternate their chunk order (default 1), 7 = two tile
+ * rows per warp in the 16-row two-sweep pass (k_sweep2p; bitwise unchanged). */
 int psg_set_option(psg_slab* s, int option, int value);
 
 /* Enable / disable two sweeps per HBM pass (temporal blocking) for pairs of

@@ -139,6 +139,10 @@ class Slab:
         """Two-sweep passes alternate their chunk order (default 1)."""
         self.set_option(6, on)
 
+    def set_t2_pairs(self, on: int):
+        """Two tile rows per warp in the 16-row two-sweep pass (k_sweep2p)."""
+        self.set_option(7, on)
+
     def set_coef_check(self, on: int):
         """Always take the range-checked coefficient path (default: only when needed)."""
         self.set_option(4, on)

@@ -149,8 +149,8 @@ def test_march_matches_single_step_sweeps(gpu_lib, n, steps, every):
 
 @pytest.mark.parametrize("n,steps,every", [(8, 9, 0), (16, 50, 0), (40, 123, 20), (64, 300, 100),
                                            (100, 61, 0), (130, 64, 30), (256, 20, 10)])
-@pytest.mark.parametrize("rows,stages", [(8, 6), (16, 6), (16, 9)])
-def test_two_step_pass_matches_single_steps(gpu_lib, n, steps, every, rows, stages):
+@pytest.mark.parametrize("rows,stages,pairs", [(8, 6, 0), (16, 6, 0), (16, 9, 0), (16, 6, 1)])
+def test_two_step_pass_matches_single_steps(gpu_lib, n, steps, every, rows, stages, pairs):
     """Temporal blocking (two sweeps per HBM pass, intermediate plane ring in
     shared memory) gives the same bits as one launch per sweep."""
     spec = LatticeSpec(N=n, a=0.3, m=1.0, dtau=0.3 * 0.3 / 4.0)
@@ -167,6 +167,7 @@ def test_two_step_pass_matches_single_steps(gpu_lib, n, steps, every, rows, stag
             s.set_temporal(t2)
             s.set_t2_rows(rows)
             s.set_t2_stages(stages)
+            s.set_t2_pairs(pairs)
             s.set_field(psi0)
             s.set_potential(v)
             idx, sums, status = s.run(steps, measure_every=every, norm_every=every)
@@ -179,8 +180,8 @@ def test_two_step_pass_matches_single_steps(gpu_lib, n, steps, every, rows, stag
 
 @pytest.mark.parametrize("n,rows,wide,force", [(40, 16, False, True), (72, 16, True, False),
                                                (72, 8, True, False), (130, 16, True, True)])
-@pytest.mark.parametrize("stages", [6, 9])
-def test_two_step_pass_coefficient_paths(gpu_lib, n, rows, wide, force, stages):
+@pytest.mark.parametrize("stages,pairs", [(6, 0), (9, 0), (6, 1)])
+def test_two_step_pass_coefficient_paths(gpu_lib, n, rows, wide, force, stages, pairs):
     """The two-step pass's coefficient paths: without the per-plane range vote
     (every d = 1 + hV in [0.25, 4), checked at upload), with it (option 4),
     and potentials reaching d >= 4 or d < 0.25 (IEEE division per site) all
@@ -205,6 +206,7 @@ def test_two_step_pass_coefficient_paths(gpu_lib, n, rows, wide, force, stages):
             s.set_t2_rows(rows)
             s.set_option(4, 1 if force else 0)
             s.set_t2_stages(stages)
+            s.set_t2_pairs(pairs)
             s.set_field(psi0)
             s.set_potential(v)
             idx, sums, status = s.run(40, measure_every=20, norm_every=20)
