@@ -367,7 +367,10 @@ int psg_tune(psg_slab* s, int blocks_per_sm, int zchunk, int stages);
  * block per SM, default; bitwise unchanged), 4 = always take the range-checked
  * coefficient path, 5 = TMA stages of the 16-row two-sweep pass (6 or 9),
  * 6 = two-sweep passes alternate their chunk order (default 1), 7 = two tile
- * rows per warp in the 16-row two-sweep pass (k_sweep2p; bitwise unchanged). */
+ * rows per warp in the 16-row two-sweep pass (k_sweep2p; bitwise unchanged),
+ * 8 = work split of the two-sweep pass: 0 automatic (default), 1 round-robin
+ * chunk items, 2 one contiguous (tile, plane) range per block (bitwise
+ * unchanged). */
 int psg_set_option(psg_slab* s, int option, int value);
 
 /* Enable / disable two sweeps per HBM pass (temporal blocking) for pairs of

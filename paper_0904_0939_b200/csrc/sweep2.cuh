@@ -167,6 +167,41 @@ __device__ __forceinline__ T2Item t2b_item(const SweepArgs& a, int item) {
   return r;
 }
 
+// The items of this block, in order.  Chunk mode: items blockIdx.x,
+// blockIdx.x + gridDim.x, ... of the chunk-major list.  Segment mode
+// (args.seg): block b owns the range [b T / G, (b+1) T / G) of the sequence
+// of T = tiles x planes (tile, plane) pairs, tiles row-band major, split at
+// tile boundaries.  With G a multiple of the tile rows, the block holding
+// (tile, z) and the one holding its j-neighbour (tile +- tiles_k, z) are
+// exactly G / tiles_j blocks apart and reach z at the same time, so the
+// psi halo rows they share are read once from DRAM; every block marches
+// about T / G planes with at most two z-halo restarts.
+template <int TB, typename F>
+__device__ __forceinline__ void t2b_for_items(const SweepArgs& a, F&& f) {
+  if (!a.seg) {
+    for (int item = blockIdx.x; item < a.nitems; item += gridDim.x) f(t2b_item<TB>(a, item));
+    return;
+  }
+  const int np = a.z_hi - a.z_lo + 1;
+  const long long total = (long long)a.tiles * np;
+  long long pos = total * blockIdx.x / gridDim.x;
+  const long long end = total * (blockIdx.x + 1) / gridDim.x;
+  while (pos < end) {
+    const int tile = (int)(pos / np);
+    const int zz = (int)(pos - (long long)tile * np);
+    const int len = (int)min((long long)(np - zz), end - pos);
+    const int tj = tile / a.tiles_k;
+    T2Item r;
+    r.idx = 0x7fffffff;   // no signalled items in segment mode
+    r.z0 = a.z_lo + zz;
+    r.z1 = r.z0 + len - 1;
+    r.j = 1 + tj * TB;
+    r.k = 1 + (tile - tj * a.tiles_k) * TX;
+    f(r);
+    pos += len;
+  }
+}
+
 // a work item whose step-1 region (tile rows j0-1 .. j0+TB, columns k0-1 ..
 // k0+64, global planes x_off+z0-1 .. x_off+z1+1) lies inside the lattice
 // needs no site masks
@@ -314,17 +349,12 @@ __device__ __forceinline__ void t2b_rows(const SweepArgs& args, uint32_t sm0, in
   const uint32_t base = sm0 + (uint32_t)(((w + 1) * BOXW + 2 * lane + 2) * 8);
   StageCursor<S> nx;
   uint32_t g = 4;   // ring plane counter (runs across items; 0..3 are the pre-completed phases)
-  for (int item = blockIdx.x; item < args.nitems; item += gridDim.x) {
-    const T2Item I = t2b_item<TB>(args, item);
-#if defined(PSG_TILE_MASK)
-    if (t2b_interior<TB>(I, args.n, args.x_off))
-#else
+  t2b_for_items<TB>(args, [&](const T2Item& I) {
     if (t2b_row_interior(I, w, args.n, args.x_off))
-#endif
       t2b_rows_item<S, TB, STEP2, FASTC, false>(args, I, fb, base, w, lane, nx, g);
     else
       t2b_rows_item<S, TB, STEP2, FASTC, true>(args, I, fb, base, w, lane, nx, g);
-  }
+  });
 }
 
 template <int S, int TB, bool FASTC, bool MASK>
@@ -403,17 +433,12 @@ __device__ __forceinline__ void t2b_ringw(const SweepArgs& args, uint32_t sm0, i
   const uint32_t base = sm0 + (uint32_t)(((rrow + 1) * BOXW + rcol) * 8);
   StageCursor<S> nx;
   uint32_t g = 4;
-  for (int item = blockIdx.x; item < args.nitems; item += gridDim.x) {
-    const T2Item I = t2b_item<TB>(args, item);
-#if defined(PSG_TILE_MASK)
-    if (t2b_interior<TB>(I, args.n, args.x_off))
-#else
+  t2b_for_items<TB>(args, [&](const T2Item& I) {
     if (t2b_ring_interior<TB>(I, args.n, args.x_off))
-#endif
       t2b_ring_item<S, TB, FASTC, false>(args, I, fb, base, rrow, rcol, active, lane, nx, g);
     else
       t2b_ring_item<S, TB, FASTC, true>(args, I, fb, base, rrow, rcol, active, lane, nx, g);
-  }
+  });
 }
 
 template <int NST, int TB, bool FASTC>
@@ -451,8 +476,7 @@ __global__ void __launch_bounds__(T2BGeo<TB>::THREADS, T2BGeo<TB>::MINB)
       tma_prefetch_desc(&tm_psi);
       tma_prefetch_desc(&tm_v);
       int it = 0;
-      for (int item = blockIdx.x; item < args.nitems; item += gridDim.x) {
-        const T2Item I = t2b_item<TB>(args, item);
+      t2b_for_items<TB>(args, [&](const T2Item& I) {
         const int kc = I.k + COL_OFF;
         for (int p = I.z0 - 2; p <= I.z1 + 2; ++p, ++it) {
           const int slot = it % S;
@@ -465,7 +489,7 @@ __global__ void __launch_bounds__(T2BGeo<TB>::THREADS, T2BGeo<TB>::MINB)
           // rows / columns from L2 (-4 % DRAM bytes, +1..2 % at 256^3..512^3)
           if (hasv) tma_load_3d(st + G::PSI_STRIDE, &tm_v, kc - 2, I.j - 1, p, &full[slot]);
         }
-      }
+      });
     }
     return;
   }

@@ -195,13 +195,12 @@ __device__ __forceinline__ void t2p_rows(const SweepArgs& args, uint32_t sm0, in
   const uint32_t boff = (uint32_t)((eb - ea) * BOXW * 8);
   StageCursor<S> nx;
   uint32_t g = 4;   // ring plane counter (runs across items; 0..3 are the pre-completed phases)
-  for (int item = blockIdx.x; item < args.nitems; item += gridDim.x) {
-    const T2Item I = t2b_item<16>(args, item);
+  t2b_for_items<16>(args, [&](const T2Item& I) {
     if (t2p_rows_interior(I, ea, eb, args.n, args.x_off))
       t2p_rows_item<S, TILE, FASTC, false>(args, I, fb, base, boff, ea, eb, lane, nx, g);
     else
       t2p_rows_item<S, TILE, FASTC, true>(args, I, fb, base, boff, ea, eb, lane, nx, g);
-  }
+  });
 }
 
 template <int NST, bool FASTC>
@@ -238,8 +237,7 @@ __global__ void __launch_bounds__(T2PGeo::THREADS, 1)
       tma_prefetch_desc(&tm_psi);
       tma_prefetch_desc(&tm_v);
       int it = 0;
-      for (int item = blockIdx.x; item < args.nitems; item += gridDim.x) {
-        const T2Item I = t2b_item<16>(args, item);
+      t2b_for_items<16>(args, [&](const T2Item& I) {
         const int kc = I.k + COL_OFF;
         for (int p = I.z0 - 2; p <= I.z1 + 2; ++p, ++it) {
           const int slot = it % S;
@@ -250,7 +248,7 @@ __global__ void __launch_bounds__(T2PGeo::THREADS, 1)
           tma_load_3d(st, &tm_psi, kc - 2, I.j - 2, p + 1, &full[slot]);   // deep-halo map: plane + 1
           if (hasv) tma_load_3d(st + G::PSI_STRIDE, &tm_v, kc - 2, I.j - 1, p, &full[slot]);
         }
-      }
+      });
     }
     return;
   }

@@ -143,6 +143,11 @@ class Slab:
         """Two tile rows per warp in the 16-row two-sweep pass (k_sweep2p)."""
         self.set_option(7, on)
 
+    def set_t2_seg(self, mode: int):
+        """Work split of the two-sweep pass: 0 automatic, 1 round-robin chunk
+        items, 2 one contiguous (tile, plane) range per block."""
+        self.set_option(8, mode)
+
     def set_coef_check(self, on: int):
         """Always take the range-checked coefficient path (default: only when needed)."""
         self.set_option(4, on)

@@ -149,8 +149,10 @@ def test_march_matches_single_step_sweeps(gpu_lib, n, steps, every):
 
 @pytest.mark.parametrize("n,steps,every", [(8, 9, 0), (16, 50, 0), (40, 123, 20), (64, 300, 100),
                                            (100, 61, 0), (130, 64, 30), (256, 20, 10)])
-@pytest.mark.parametrize("rows,stages,pairs", [(8, 6, 0), (16, 6, 0), (16, 9, 0), (16, 6, 1)])
-def test_two_step_pass_matches_single_steps(gpu_lib, n, steps, every, rows, stages, pairs):
+@pytest.mark.parametrize("rows,stages,pairs,seg", [(8, 6, 0, 1), (16, 6, 0, 1), (16, 9, 0, 1),
+                                                   (16, 6, 1, 1), (16, 6, 0, 2), (16, 6, 1, 2),
+                                                   (16, 6, 0, 0)])
+def test_two_step_pass_matches_single_steps(gpu_lib, n, steps, every, rows, stages, pairs, seg):
     """Temporal blocking (two sweeps per HBM pass, intermediate plane ring in
     shared memory) gives the same bits as one launch per sweep."""
     spec = LatticeSpec(N=n, a=0.3, m=1.0, dtau=0.3 * 0.3 / 4.0)
@@ -168,6 +170,7 @@ def test_two_step_pass_matches_single_steps(gpu_lib, n, steps, every, rows, stag
             s.set_t2_rows(rows)
             s.set_t2_stages(stages)
             s.set_t2_pairs(pairs)
+            s.set_t2_seg(seg)
             s.set_field(psi0)
             s.set_potential(v)
             idx, sums, status = s.run(steps, measure_every=every, norm_every=every)
