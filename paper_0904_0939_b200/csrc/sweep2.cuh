@@ -108,6 +108,46 @@ struct StageCursor {
   }
 };
 
+// consumer cursor over the TMA stages that rotates the lane's shared-memory
+// address in the stage and the stage's full barrier by adds (no slot
+// multiplies in the plane loop); persists across work items
+template <int S, uint32_t STAGE>
+struct StageRot {
+  uint32_t addr, bar, ph;
+  __device__ __forceinline__ StageRot(uint32_t base, uint32_t fb) : addr(base), bar(fb), ph(0) {}
+  __device__ __forceinline__ void next(uint32_t base, uint32_t fb) {
+    addr += STAGE;
+    bar += 8;
+    if (bar == fb + S * 8) {
+      addr = base;
+      bar = fb;
+      ph ^= 1u;
+    }
+  }
+};
+
+// psi' ring slots of plane g (write) and g-1 (read): byte offsets, rfull
+// barriers and the read phase parity, rotating mod 4 inside an item
+template <uint32_t RING>
+struct RingRot {
+  uint32_t rw, rr, bw, br, rph;
+  __device__ __forceinline__ RingRot(uint32_t g, uint32_t rf0) {
+    rw = (g & 3u) * RING;
+    rr = ((g - 1) & 3u) * RING;
+    bw = rf0 + (g & 3u) * 8;
+    br = rf0 + ((g - 1) & 3u) * 8;
+    rph = ((g - 1) >> 2) & 1u;
+  }
+  __device__ __forceinline__ void next(uint32_t rf0) {
+    rr = rw;
+    br = bw;
+    const bool wrap = rw == 3 * RING;
+    rw = wrap ? 0u : rw + RING;
+    bw = wrap ? rf0 : bw + 8;
+    rph ^= br == rf0 ? 1u : 0u;   // plane g-1 starts a new lap of the 4 slots
+  }
+};
+
 struct T2Item {
   int z0, z1, j, k, idx;
 };
@@ -178,6 +218,8 @@ __device__ __forceinline__ T2Item t2b_item(const SweepArgs& a, int item) {
 // about T / G planes with at most two z-halo restarts.
 template <int TB, typename F>
 __device__ __forceinline__ void t2b_for_items(const SweepArgs& a, F&& f) {
+  // two loops (the body is inlined in each; only one runs per launch): a
+  // shared loop with the mode test per item measured 3 % slower at 128^3
   if (!a.seg) {
     for (int item = blockIdx.x; item < a.nitems; item += gridDim.x) f(t2b_item<TB>(a, item));
     return;
@@ -231,11 +273,12 @@ __device__ __forceinline__ bool t2b_ring_interior(const T2Item& I, int n, int x_
 template <int S, int TB, bool STEP2, bool FASTC, bool MASK>
 __device__ __forceinline__ void t2b_rows_item(const SweepArgs& args, const T2Item& I,
                                               uint32_t fb, uint32_t base, int w, int lane,
-                                              StageCursor<S>& nx, uint32_t& g) {
+                                              StageRot<S, T2BGeo<TB>::STAGE>& nx, uint32_t& g) {
   using G = T2BGeo<TB>;
   using C = T2BCfg<S, TB>;
   constexpr uint32_t VOFF = G::PSI_STRIDE - BOXW * 8;  // V box starts one row lower
   constexpr uint32_t ROFF = C::RING_OFF - BOXW * 8;    // ring holds E rows
+  const uint32_t rf0 = fb + 2 * S * 8;                 // rfull[0]
   const int n = args.n;
   const double h = args.h, c0 = args.c0;
   const int j = I.j - 1 + w;
@@ -250,19 +293,16 @@ __device__ __forceinline__ void t2b_rows_item(const SweepArgs& args, const T2Ite
   uint32_t doff = (uint32_t)((long long)(I.z0 - 2) * args.plane_stride + (long long)j * args.pitch +
                              (k + COL_OFF));
   const uint32_t pstride = (uint32_t)args.plane_stride;
-  // ring slot byte offsets of planes g (write) and g-1 (read), and the rfull
-  // barrier of slot g, rotating mod 4
-  uint32_t rw = (g & 3u) * G::RING, rr = ((g - 1) & 3u) * G::RING;
-  constexpr uint32_t RB_END = 4 * G::RING;
-  mbar_wait_u(fb + nx.slot * 8, nx.ph);
-  double2 c_a = lds2_u(base + nx.slot * G::STAGE);
-  mbar_arrive_u(fb + (S + nx.slot) * 8);   // every lane arrives (count 32 per warp)
-  nx.next();
-  mbar_wait_u(fb + nx.slot * 8, nx.ph);
-  double2 c_b = lds2_u(base + nx.slot * G::STAGE);
-  int cur = nx.slot;
-  nx.next();
-  bool okf = mbar_test_u(fb + nx.slot * 8, nx.ph);   // stage of the first loop plane
+  RingRot<G::RING> rg(g, rf0);
+  mbar_wait_u(nx.bar, nx.ph);
+  double2 c_a = lds2_u(nx.addr);
+  mbar_arrive_u(nx.bar + S * 8);   // every lane arrives on empty (count 32 per warp)
+  nx.next(base, fb);
+  mbar_wait_u(nx.bar, nx.ph);
+  double2 c_b = lds2_u(nx.addr);
+  uint32_t cur = nx.addr, cur_bar = nx.bar;
+  nx.next(base, fb);
+  bool okf = mbar_test_u(nx.bar, nx.ph);   // stage of the first loop plane
   double2 c_c;
   double2 q0 = make_double2(0.0, 0.0), q1 = q0, q2 = q0;
   double2 a0 = q0, a1 = q0, a2 = q0, f0 = q0, f1 = q0, f2 = q0;
@@ -271,14 +311,12 @@ __device__ __forceinline__ void t2b_rows_item(const SweepArgs& args, const T2Ite
   auto plane = [&](const double2& cp, const double2& cc, double2& cn, double2& qw,
                    const double2& qm, const double2& qmm, double2& aw, double2& fw,
                    const double2& am, const double2& fm) {
-    mbar_wait_if(okf, fb + nx.slot * 8, nx.ph);   // probed one plane earlier
+    mbar_wait_if(okf, nx.bar, nx.ph);   // probed one plane earlier
     // all warps' psi' of plane g-1, needed by step 2 below: probe now (ahead
     // of the shared loads, which the compiler keeps in order)
-    const uint32_t gp = g - 1;
-    const uint32_t rbar = fb + (2 * S + (gp & 3u)) * 8, rph = (gp >> 2) & 1u;
-    const bool okr = mbar_test_u(rbar, rph);
-    cn = lds2_u(base + nx.slot * G::STAGE);
-    const uint32_t sc = base + cur * G::STAGE;
+    const bool okr = mbar_test_u(rg.br, rg.rph);
+    cn = lds2_u(nx.addr);
+    const uint32_t sc = cur;
     const double2 jm = lds2_u(sc - BOXW * 8);
     const double2 jp = lds2_u(sc + BOXW * 8);
     const double km = lds1_u(sc - 8);
@@ -294,17 +332,18 @@ __device__ __forceinline__ void t2b_rows_item(const SweepArgs& args, const T2Ite
     } else {
       qw = make_double2(u0, u1);
     }
-    sts2_u(base + ROFF + rw, qw);
-    mbar_arrive_u(fb + (S + cur) * 8);
-    mbar_arrive_u(fb + (2 * S + (g & 3u)) * 8);
-    cur = nx.slot;
-    nx.next();
-    okf = mbar_test_u(fb + nx.slot * 8, nx.ph);   // the next plane's stage
+    sts2_u(base + ROFF + rg.rw, qw);
+    mbar_arrive_u(cur_bar + S * 8);
+    mbar_arrive_u(rg.bw);
+    cur = nx.addr;
+    cur_bar = nx.bar;
+    nx.next(base, fb);
+    okf = mbar_test_u(nx.bar, nx.ph);   // the next plane's stage
     // (the kernel's first plane waits on a pre-completed phase; no item
     // stores or computes step 2 in its first two planes)
-    mbar_wait_if(okr, rbar, rph);
+    mbar_wait_if(okr, rg.br, rg.rph);
     if (STEP2 && p > I.z0) {   // plane p-1 >= z0: an output plane of this item
-      const uint32_t rq = base + ROFF + rr;
+      const uint32_t rq = base + ROFF + rg.rr;
       const double2 rjm = lds2_u(rq - BOXW * 8);
       const double2 rjp = lds2_u(rq + BOXW * 8);
       const double rkm = lds1_u(rq - 8);
@@ -319,10 +358,8 @@ __device__ __forceinline__ void t2b_rows_item(const SweepArgs& args, const T2Ite
       }
     }
     if (STEP2) doff += pstride;
-    rr = rw;
-    rw = rw + G::RING == RB_END ? 0u : rw + G::RING;
+    rg.next(rf0);
     ++p;
-    ++g;
   };
   for (;;) {
     plane(c_a, c_b, c_c, q0, q2, q1, a0, f0, a2, f2);
@@ -332,7 +369,8 @@ __device__ __forceinline__ void t2b_rows_item(const SweepArgs& args, const T2Ite
     plane(c_c, c_a, c_b, q2, q1, q0, a2, f2, a1, f1);
     if (p == pend) break;
   }
-  mbar_arrive_u(fb + (S + cur) * 8);
+  g += (uint32_t)(pend - (I.z0 - 1));
+  mbar_arrive_u(cur_bar + S * 8);
   if (STEP2 && I.idx < args.sig_items) {
     // an edge item's planes are stored: make them visible, then count this
     // warp done (the exchange waits for the count on its own stream)
@@ -347,7 +385,7 @@ __device__ __forceinline__ void t2b_rows(const SweepArgs& args, uint32_t sm0, in
   using C = T2BCfg<S, TB>;
   const uint32_t fb = sm0 + C::BAR_OFF;               // full[S], empty[S], rfull[4]
   const uint32_t base = sm0 + (uint32_t)(((w + 1) * BOXW + 2 * lane + 2) * 8);
-  StageCursor<S> nx;
+  StageRot<S, T2BGeo<TB>::STAGE> nx(base, fb);
   uint32_t g = 4;   // ring plane counter (runs across items; 0..3 are the pre-completed phases)
   t2b_for_items<TB>(args, [&](const T2Item& I) {
     if (t2b_row_interior(I, w, args.n, args.x_off))
@@ -360,35 +398,36 @@ __device__ __forceinline__ void t2b_rows(const SweepArgs& args, uint32_t sm0, in
 template <int S, int TB, bool FASTC, bool MASK>
 __device__ __forceinline__ void t2b_ring_item(const SweepArgs& args, const T2Item& I, uint32_t fb,
                                               uint32_t base, int rrow, int rcol, bool active,
-                                              int lane, StageCursor<S>& nx, uint32_t& g) {
+                                              int lane, StageRot<S, T2BGeo<TB>::STAGE>& nx,
+                                              uint32_t& g) {
   using G = T2BGeo<TB>;
   using C = T2BCfg<S, TB>;
   constexpr uint32_t VOFF = G::PSI_STRIDE - BOXW * 8;
   constexpr uint32_t ROFF = C::RING_OFF - BOXW * 8;
+  const uint32_t rf0 = fb + 2 * S * 8;
   const int n = args.n;
   const double h = args.h, c0 = args.c0;
   const int j = I.j - 1 + rrow;
   const int k = I.k - 2 + rcol;
   const bool in0 = active & (j <= n) & ((unsigned)(k - 1) < (unsigned)n);
-  mbar_wait_u(fb + nx.slot * 8, nx.ph);
-  double c_a = lds1_u(base + nx.slot * G::STAGE);
-  mbar_arrive_u(fb + (S + nx.slot) * 8);   // every lane arrives (count 32 per warp)
-  nx.next();
-  mbar_wait_u(fb + nx.slot * 8, nx.ph);
-  double c_b = lds1_u(base + nx.slot * G::STAGE);
-  int cur = nx.slot;
-  nx.next();
-  bool okf = mbar_test_u(fb + nx.slot * 8, nx.ph);
+  RingRot<G::RING> rg(g, rf0);
+  mbar_wait_u(nx.bar, nx.ph);
+  double c_a = lds1_u(nx.addr);
+  mbar_arrive_u(nx.bar + S * 8);   // every lane arrives on empty (count 32 per warp)
+  nx.next(base, fb);
+  mbar_wait_u(nx.bar, nx.ph);
+  double c_b = lds1_u(nx.addr);
+  uint32_t cur = nx.addr, cur_bar = nx.bar;
+  nx.next(base, fb);
+  bool okf = mbar_test_u(nx.bar, nx.ph);
   double c_c;
   const int pend = I.z1 + 2;
   int p = I.z0 - 1;
   auto plane = [&](const double& cp, const double& cc, double& cn) {
-    mbar_wait_if(okf, fb + nx.slot * 8, nx.ph);
-    const uint32_t gp = g - 1;
-    const uint32_t rbar = fb + (2 * S + (gp & 3u)) * 8, rph = (gp >> 2) & 1u;
-    const bool okr = mbar_test_u(rbar, rph);
-    cn = lds1_u(base + nx.slot * G::STAGE);
-    const uint32_t sc = base + cur * G::STAGE;
+    mbar_wait_if(okf, nx.bar, nx.ph);
+    const bool okr = mbar_test_u(rg.br, rg.rph);
+    cn = lds1_u(nx.addr);
+    const uint32_t sc = cur;
     const double jm = lds1_u(sc - BOXW * 8);
     const double jp = lds1_u(sc + BOXW * 8);
     const double km = lds1_u(sc - 8);
@@ -402,15 +441,16 @@ __device__ __forceinline__ void t2b_ring_item(const SweepArgs& args, const T2Ite
       const bool pin = (unsigned)(args.x_off + p - 1) < (unsigned)n;   // global plane
       qv = (pin & in0) ? u : cc;
     }
-    if (active) sts1_u(base + ROFF + (g & 3u) * G::RING, qv);
-    mbar_arrive_u(fb + (S + cur) * 8);
-    mbar_arrive_u(fb + (2 * S + (g & 3u)) * 8);
-    cur = nx.slot;
-    nx.next();
-    okf = mbar_test_u(fb + nx.slot * 8, nx.ph);
-    mbar_wait_if(okr, rbar, rph);
+    if (active) sts1_u(base + ROFF + rg.rw, qv);
+    mbar_arrive_u(cur_bar + S * 8);
+    mbar_arrive_u(rg.bw);
+    cur = nx.addr;
+    cur_bar = nx.bar;
+    nx.next(base, fb);
+    okf = mbar_test_u(nx.bar, nx.ph);
+    mbar_wait_if(okr, rg.br, rg.rph);
+    rg.next(rf0);
     ++p;
-    ++g;
   };
   for (;;) {
     plane(c_a, c_b, c_c);
@@ -420,7 +460,8 @@ __device__ __forceinline__ void t2b_ring_item(const SweepArgs& args, const T2Ite
     plane(c_c, c_a, c_b);
     if (p == pend) break;
   }
-  mbar_arrive_u(fb + (S + cur) * 8);
+  g += (uint32_t)(pend - (I.z0 - 1));
+  mbar_arrive_u(cur_bar + S * 8);
 }
 
 template <int S, int TB, bool FASTC>
@@ -431,7 +472,7 @@ __device__ __forceinline__ void t2b_ringw(const SweepArgs& args, uint32_t sm0, i
   const int rcol = lane < TB ? 1 : 66;
   const bool active = lane < 2 * TB;
   const uint32_t base = sm0 + (uint32_t)(((rrow + 1) * BOXW + rcol) * 8);
-  StageCursor<S> nx;
+  StageRot<S, T2BGeo<TB>::STAGE> nx(base, fb);
   uint32_t g = 4;
   t2b_for_items<TB>(args, [&](const T2Item& I) {
     if (t2b_ring_interior<TB>(I, args.n, args.x_off))

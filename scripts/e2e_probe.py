@@ -35,3 +35,13 @@ for rep in range(3):
     names = ["Slab()", "dirichlet check", "set_field H2D", "set_potential H2D+check", "run 4000",
              "get_field D2H", "close"]
     print(" | ".join(f"{nm} {1e3 * (b - a):.1f} ms" for nm, a, b in zip(names, t, t[1:])), flush=True)
+
+# the public call itself, interleaved with the hand-composed sequence above
+from paper_0904_0939_b200 import evolve_fixed  # noqa: E402
+
+for rep in range(4):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    st = evolve_fixed(init, grid, 4000, 500, norm_every=500)
+    t1 = time.perf_counter()
+    print(f"evolve_fixed {1e3 * (t1 - t0):.1f} ms", flush=True)
