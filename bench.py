@@ -392,6 +392,97 @@ def run_single(args):
     print(json.dumps(line), flush=True)
 
 
+def run_large(args):
+    """One GPU, lattices whose host arrays do not fit the bench's pinned
+    buffers (C5: 2048^3, 69 GB per field).  Start field and potential are
+    generated on the device (bitwise the host recipes, workloads.fill_slab) and
+    the slab is single-buffer (psi 77.9 GB + V 69.1 GB at 2048^3; two psi
+    buffers would need 207 GB).  Same timed region and roofline method as
+    run_single; no e2e leg (the inputs never exist on the host)."""
+    import torch
+
+    from paper_0904_0939_b200 import workloads
+    from paper_0904_0939_b200.device import Slab
+
+    w = workload(args.config)
+    if args.size:
+        w = workloads.scaled(w, args.size)
+    spec = w.spec
+    n = spec.N
+    dev = 0
+    torch.cuda.set_device(dev)
+    slab = Slab(spec, device=dev, single_buffer=True, chunk=args.chunk)
+    t0 = time.perf_counter()
+    workloads.fill_slab(slab, w)
+    slab.sync()
+    fill_s = time.perf_counter() - t0
+    st = torch.cuda.ExternalStream(slab.stream)
+    m = w.measure_every
+    slab.run(args.warmup, measure_every=m, norm_every=m)
+    slab.sync()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0 = slab.launches()
+    with ClockSampler(dev) as clk:
+        torch.cuda.synchronize()
+        e0.record(st)
+        idx, sums, status = slab.run(args.steps, measure_every=m, norm_every=m,
+                                     step_offset=args.warmup)
+        e1.record(st)
+        e1.synchronize()
+        torch.cuda.synchronize()
+    launches = slab.launches() - l0
+    ms = e0.elapsed_time(e1)
+    clocks = clk.summary()
+    if status.any():
+        raise SystemExit(f"device status {status} during the timed run")
+    value = n ** 3 * args.steps / (ms * 1e-3) / 1e9
+    # dominant kernel: plain pairs (one two-sweep pass over the lattice = its
+    # chunk launches), timed back to back as in the timed region
+    npass, nsingle = t2_schedule(args.steps, args.warmup, m)
+    l_probe = slab.launches()
+    slab.run(2, 0, 0)
+    slab.sync()
+    per_pass = slab.launches() - l_probe
+    ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = max(4, min(npass, 40))
+    ea.record(st)
+    slab.run(2 * reps, 0, 0)
+    eb.record(st)
+    eb.synchronize()
+    pass_s = ea.elapsed_time(eb) * 1e-3 / reps
+    fbytes = slab.field_bytes
+    slab.close()
+    peak, peak_kind = hbm_peak()
+    achieved = BYTES_PER_SITE * n ** 3 / pass_s / 1e9
+    line = {
+        "metric": "fp64 FDTD lattice-site updates/s (GLUPS)",
+        "value": value, "unit": "GLUPS", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": w.name, "N": n, "a": spec.a, "dtau": spec.dtau,
+                   "potential": w.potential, "measure_every": m, "norm_every": m,
+                   "l2": "fields (%.1f GB) larger than L2; no flush" % (fbytes / 1e9),
+                   "parallelism": "single GPU, single-buffer slab",
+                   "inputs": "device-generated (workloads.fill_slab), %.1f s" % fill_s,
+                   "field_bytes": fbytes},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None,
+                     "kernel": "k_sweep2b (two fp64 7-point sweeps per HBM pass), "
+                               f"{per_pass} chunk launches per pass",
+                     "pass_us": pass_s * 1e6, "peak_source": peak_kind,
+                     "algorithmic_bytes_per_pass": BYTES_PER_SITE * n ** 3,
+                     "site_updates_per_pass": 2 * n ** 3,
+                     "share_of_timed_region": npass * pass_s / (ms * 1e-3)},
+        "clocks": clocks,
+        "e2e": None,
+        "e2e_note": "inputs generated in HBM (no host arrays at this size): no end-to-end number",
+        "gpu_launches": launches,
+        "cpu_baseline": None,
+        "observables": {"E": [float(np.sum(sm[0]) / np.sum(sm[1])) for sm in sums]},
+    }
+    print(json.dumps(line), flush=True)
+
+
 def t2_schedule(steps: int, offset: int, m: int):
     """(two-sweep passes, single sweeps) psg_run issues for a fixed run with
     measure / norm every m (the pairing rule of run_loop in csrc/psigpu.cu:
@@ -563,6 +654,10 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="C2")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--single-buffer", action="store_true",
+                    help="one GPU, single-buffer slab, device-generated inputs (default for C5)")
+    ap.add_argument("--size", type=int, default=0, help="rescale the config's lattice (with --single-buffer)")
+    ap.add_argument("--chunk", type=int, default=0, help="planes per chunk launch of a single-buffer slab")
     ap.add_argument("--dist", action="store_true",
                     help="use the torch.distributed slab engine even for one rank (testing)")
     args = ap.parse_args()
@@ -572,6 +667,8 @@ def main():
         return run_reference(args)
     if int(os.environ.get("WORLD_SIZE", "1")) > 1 or args.dist:
         return run_dist(args)
+    if args.single_buffer or args.config == "C5":
+        return run_large(args)
     return run_single(args)
 
 

@@ -152,7 +152,25 @@ typedef struct psg_comm psg_comm;
  * and parallel.Worker (parallel.py:125-176). */
 int psg_create(int device, int64_t n, int64_t w, int64_t x_lo, double a, double m, double dtau,
                psg_slab** out);
+
+/* psg_create with options.  PSG_CREATE_SINGLE_BUFFER (whole lattice only,
+ * w == n): both psi "buffers" share one allocation of w + 4 + chunk + 2
+ * planes instead of 2 (w + 4), the second shifted `chunk + 2` planes below
+ * the first; every sweep / two-sweep pass runs as launches over `chunk`-plane
+ * pieces, ascending into the lower buffer and descending into the upper one,
+ * so no piece overwrites a plane a later piece still reads.  Results are
+ * bitwise those of psg_create.  chunk = 0: ceil(w / 8).  A 2048^3 lattice
+ * (psi 73.6 GB + V 69.1 GB) then fits one B200.  Not for psg_run_dist /
+ * multi-slab runs (there each GPU holds a slab with its own halos) or the
+ * persistent march.  Extends evolve.SweepBuffers (evolve.py:160-166), whose
+ * two full buffers are the reference's memory layout. */
+#define PSG_CREATE_SINGLE_BUFFER 1u
+int psg_create_ex(int device, int64_t n, int64_t w, int64_t x_lo, double a, double m, double dtau,
+                  unsigned flags, int64_t chunk, psg_slab** out);
 int psg_destroy(psg_slab* s);
+
+/* Device bytes held by the slab's psi buffers and V (fields only). */
+int64_t psg_field_bytes(psg_slab* s);
 
 /* The slab's CUDA stream (cudaStream_t as void*). */
 void* psg_stream(psg_slab* s);
@@ -370,7 +388,9 @@ int psg_tune(psg_slab* s, int blocks_per_sm, int zchunk, int stages);
  * rows per warp in the 16-row two-sweep pass (k_sweep2p; bitwise unchanged),
  * 8 = work split of the two-sweep pass: 0 automatic (default), 1 round-robin
  * chunk items, 2 one contiguous (tile, plane) range per block (bitwise
- * unchanged). */
+ * unchanged), 9 = at most this many planes per two-sweep launch (0 = as
+ * many as 32-bit output offsets allow, the default; slabs beyond that are
+ * passed in several launches; bitwise unchanged). */
 int psg_set_option(psg_slab* s, int option, int value);
 
 /* Enable / disable two sweeps per HBM pass (temporal blocking) for pairs of

@@ -77,7 +77,10 @@ SIGNATURES = {
     "psg_kernel_dot_plane_sums": (c_int, [_dp, _dp, c_int64, c_int64, c_int64, c_int64, _dp]),
     "psg_create": (c_int, [c_int, c_int64, c_int64, c_int64, c_double, c_double, c_double,
                            POINTER(c_void_p)]),
+    "psg_create_ex": (c_int, [c_int, c_int64, c_int64, c_int64, c_double, c_double, c_double,
+                              c_uint, c_int64, POINTER(c_void_p)]),
     "psg_destroy": (c_int, [c_void_p]),
+    "psg_field_bytes": (c_int64, [c_void_p]),
     "psg_stream": (c_void_p, [c_void_p]),
     "psg_sync": (c_int, [c_void_p]),
     "psg_geometry": (c_int, [c_void_p, _lp, _lp, _lp]),

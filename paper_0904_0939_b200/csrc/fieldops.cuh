@@ -81,6 +81,48 @@ __global__ void k_impose(const double* __restrict__ in, double* __restrict__ out
   }
 }
 
+// k_impose in place (single-buffer slabs): one thread per mirror pair
+// (c, n+1-c) along `axis` reads both sites before writing either, so the
+// values are those of k_impose (same operations per site)
+__global__ void k_impose_pairs(double* f, const double* sp, int axis, double sign, int mode, int n,
+                               int pitch, long long plane_stride) {
+  const int ext = n + 2;
+  const int hext = (n + 1) / 2 + 1;   // c = 0 .. (n+1)/2 (the centre pairs with itself for odd n)
+  const long long total = (long long)hext * ext * ext;
+  const double sc = *sp;
+  const int half = n / 2;
+  const int first_target = n - half + 1;
+  const bool zero_center = (n % 2 == 1) && sign < 0.0;
+  const int center = (n + 1) / 2;
+  const long long st[3] = {plane_stride, (long long)pitch, 1};
+  auto val = [&](int ci, double self, double mir) {
+    if (mode != 0) return __dmul_rn(__dadd_rn(self, __dmul_rn(sign, mir)), 0.5);
+    if (ci >= first_target && ci <= n) return __dmul_rn(sign, mir);
+    if (zero_center && ci == center) return 0.0;
+    return self;
+  };
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    // t enumerates (c, u, v): c along `axis`, u, v the other two axes in order
+    const int v = (int)(t % ext);
+    const long long r = t / ext;
+    const int u = (int)(r % ext);
+    const int c = (int)(r / ext);
+    const int m = n + 1 - c;
+    int ax[3], q = 0;
+    for (int d = 0; d < 3; ++d) ax[d] = d == axis ? -1 : (q++ == 0 ? u : v);
+    long long base = COL_OFF;
+    for (int d = 0; d < 3; ++d)
+      if (d != axis) base += (long long)ax[d] * st[d];
+    const long long pc = base + (long long)c * st[axis];
+    const long long pm = base + (long long)m * st[axis];
+    const double xc = __dmul_rn(f[pc], sc);
+    const double xm = __dmul_rn(f[pm], sc);
+    f[pc] = val(c, xc, xm);
+    if (m != c) f[pm] = val(m, xm, xc);
+  }
+}
+
 // trilinear resample, bitwise replica of multires._axis_interp applied along
 // axis 0, then 1, then 2: each lerp is lo + f*(hi - lo)
 __global__ void k_resample(const double* __restrict__ coarse, const double* csp, int nc,

@@ -290,7 +290,7 @@ __device__ __forceinline__ void t2b_rows_item(const SweepArgs& args, const T2Ite
   const bool ok1 = (j <= n) & (k + 1 <= n);
   // element offset of this lane's output pair (fields < 2^32 elements, checked
   // on the host): one 32-bit add per plane instead of 64-bit pointer math
-  uint32_t doff = (uint32_t)((long long)(I.z0 - 2) * args.plane_stride + (long long)j * args.pitch +
+  uint32_t doff = (uint32_t)((long long)(I.z0 - 2 - args.z_base) * args.plane_stride + (long long)j * args.pitch +
                              (k + COL_OFF));
   const uint32_t pstride = (uint32_t)args.plane_stride;
   RingRot<G::RING> rg(g, rf0);

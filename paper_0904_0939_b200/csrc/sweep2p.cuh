@@ -59,7 +59,7 @@ __device__ __forceinline__ void t2p_rows_item(const SweepArgs& args, const T2Ite
   const bool oka0 = (ja <= n) & (k <= n), oka1 = (ja <= n) & (k + 1 <= n);
   const bool okb0 = (jb <= n) & (k <= n), okb1 = (jb <= n) & (k + 1 <= n);
   // element offset of row a's output pair (row b: + pitch)
-  uint32_t doff = (uint32_t)((long long)(I.z0 - 2) * args.plane_stride + (long long)ja * args.pitch +
+  uint32_t doff = (uint32_t)((long long)(I.z0 - 2 - args.z_base) * args.plane_stride + (long long)ja * args.pitch +
                              (k + COL_OFF));
   const uint32_t pstride = (uint32_t)args.plane_stride;
   const uint32_t pitch = (uint32_t)args.pitch;

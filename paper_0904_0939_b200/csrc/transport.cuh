@@ -383,7 +383,7 @@ int run_loop(std::vector<psg_slab*>& sl, Transport* tr, const psg_run_params* p,
   // planes per face); the march only for a whole lattice
   bool t2_ok = true;
   for (psg_slab* s : sl)
-    t2_ok = t2_ok && s->use_t2 && !s->use_ac && (!tr || s->w >= 2) && s->field_elems < (1ull << 32);
+    t2_ok = t2_ok && s->use_t2 && !s->use_ac && (!tr || s->w >= 2);
   const bool whole = !tr;
   auto set_all = [&](auto&& f) {
     for (psg_slab* s : sl) {

@@ -64,7 +64,8 @@ def pinned_empty(shape) -> np.ndarray:
 class Slab:
     """One GPU's slab of local planes 0..w+1 (global x_lo-1 .. x_lo+w)."""
 
-    def __init__(self, spec: LatticeSpec, w: int | None = None, x_lo: int = 1, device: int = 0):
+    def __init__(self, spec: LatticeSpec, w: int | None = None, x_lo: int = 1, device: int = 0,
+                 single_buffer: bool = False, chunk: int = 0):
         lib = _lib.load()
         if lib.psg_device_count() <= 0:
             raise DeviceError("no CUDA device visible: the hot path has no CPU fallback")
@@ -74,14 +75,23 @@ class Slab:
         self.x_lo = int(x_lo)
         self.device = device
         h = ctypes.c_void_p()
-        check(lib.psg_create(device, self.n, self.w, self.x_lo, spec.a, spec.m, spec.dtau,
-                             ctypes.byref(h)))
+        # single_buffer: both psi buffers in one allocation, shifted by chunk + 2
+        # planes (psg_create_ex, include/psigpu.h); whole lattice only
+        self.single_buffer = bool(single_buffer)
+        flags = 1 if self.single_buffer else 0
+        check(lib.psg_create_ex(device, self.n, self.w, self.x_lo, spec.a, spec.m, spec.dtau,
+                                flags, int(chunk), ctypes.byref(h)))
         self._h = h
         self._lib = lib
         pitch, stride, planes = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
         lib.psg_geometry(h, ctypes.byref(pitch), ctypes.byref(stride), ctypes.byref(planes))
         self.pitch, self.plane_stride, self.planes = pitch.value, stride.value, planes.value
         self._v_owner = None
+
+    @property
+    def field_bytes(self) -> int:
+        """Device bytes of the psi buffers and V."""
+        return int(self._lib.psg_field_bytes(self._h))
 
     # ------------------------------------------------------------ lifetime
     def close(self):

@@ -5,8 +5,10 @@ seeded synthetic inputs of paper_0904_0939_b200.workloads, checked by
 size-independent properties (norm, parity exactness, convergence of the
 energy, physics targets up to O(a^2)) and against the CPU oracle for the
 first sweeps at full size (where the oracle finishes in seconds).
-Config 5 (2048^3, 207 GB for three fields) does not fit one GPU; its recipe
-runs at 512^3 (same box side 20, same wells) and sharded 2 ways in-process.
+Config 5 (2048^3) runs at full size on one GPU in a single-buffer slab
+(psi 77.9 GB + V 69.1 GB; two psi buffers would need 207 GB), with
+device-generated inputs; its recipe also runs at 512^3 / 1024^3 and sharded
+2 ways in-process.
 """
 
 import math
@@ -138,3 +140,59 @@ def test_c5_recipe_1024_device_inputs(gpu_lib):
         e = [float(np.sum(sm[0]) / np.sum(sm[1])) for sm in sums]
         assert all(math.isfinite(x) for x in e)
         assert all(b < a for a, b in zip(e, e[1:]))
+
+
+def _light_cone_oracle(psi_win, v_win, spec, k):
+    """k oracle sweeps of a window of planes (its edge planes held fixed):
+    the planes more than k from a window edge that is not the lattice
+    boundary are exact."""
+    cur = psi_win.copy()
+    for _ in range(k):
+        out = cur.copy()
+        O.stencil_update_v(cur, v_win, spec.dtau, spec.m, spec.a, out, 1, cur.shape[0] - 2)
+        cur = out
+    return cur
+
+
+def test_c5_2048_single_gpu(gpu_lib):
+    """BASELINE config 5 at its full size, 2048^3 x 2000 sweeps with
+    observables every 100, on ONE B200 (single-buffer slab, device inputs).
+    Parity at full size: after 4 plain sweeps (two chunked two-sweep passes),
+    sample planes equal the oracle's sweeps of their light-cone windows
+    bitwise (the windows' psi and V read back from the device).  Then the
+    whole run: finite, monotonically falling energy, unit norm."""
+    import torch
+
+    from paper_0904_0939_b200 import _lib
+    from paper_0904_0939_b200.device import Slab
+    from paper_0904_0939_b200.observables import measure_device
+
+    torch.cuda.empty_cache()
+    _lib.load().psg_trim_memory(0)
+    w = workloads.CONFIGS["C5"]
+    spec = w.spec
+    n = spec.N
+    k = 4
+    samples = [1, 3, 1024, n - 1]
+    with Slab(spec, single_buffer=True) as s:
+        workloads.fill_slab(s, w)
+        wins = []
+        for p in samples:
+            lo, hi = max(0, p - k - 1), min(n + 1, p + k + 1)
+            wins.append((p, lo, s.get_field(lo, hi - lo + 1), s.get_potential(lo, hi - lo + 1)))
+        assert np.array_equal(wins[2][2][k + 1], workloads.uniform_start(spec, first=1024, count=1)[0])
+        idx, sums, status = s.run(k, measure_every=0, norm_every=0)
+        assert not status.any()
+        for p, lo, pw, vw in wins:
+            want = _light_cone_oracle(pw, vw, spec, k)[p - lo]
+            assert np.array_equal(s.get_field(p, 1)[0], want), p
+        idx, sums, status = s.run(w.steps - k, measure_every=w.measure_every,
+                                  norm_every=w.measure_every, step_offset=k)
+        assert not status.any()
+        e = [float(np.sum(sm[0]) / np.sum(sm[1])) for sm in sums]
+        assert len(e) == (w.steps - 1) // w.measure_every
+        assert all(math.isfinite(x) for x in e)
+        assert all(b < a for a, b in zip(e, e[1:]))
+        num, den, r2 = measure_device(s)   # the final state, its pending factor applied
+        assert abs(float(np.sum(den)) * spec.a ** 3 - 1.0) < 1e-12
+        assert float(np.sum(num) / np.sum(den)) < e[-1]
