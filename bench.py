@@ -23,6 +23,11 @@ JSON fields beyond the base contract:
   e2e           the same metric through the public API (evolve_fixed) from
                 pinned host arrays: upload psi0 + V, K sweeps, download psi
                 and the observable plane sums.
+``--config C5`` (2048^3, harmonic + 8 wells): on one GPU a single-buffer slab
+with device-generated inputs (run_large; two psi buffers would need 207 GB);
+under torchrun the lattice itself is split into M slabs ("scaling": "strong",
+the north star's 1/2/4/8-GPU run).  Neither has an e2e leg: at 69 GB per field
+the inputs only ever exist in HBM.
 ``--impl reference`` times the reference algorithm's CPU implementation (the
 oracle port: the reference package is Python/numba and cannot be built into
 oracle/_ref) on the same workload.
@@ -518,6 +523,10 @@ def weak_n(n1: int, m: int) -> int:
     return max(step, int(round(n1 * m ** (1.0 / 3.0) / step)) * step)
 
 
+def strong_scaling(args) -> bool:
+    return args.config == "C5" or args.strong
+
+
 def run_dist(args):
     import torch
     import torch.distributed as dist
@@ -533,15 +542,20 @@ def run_dist(args):
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     base = workload(args.config)
+    if args.size:
+        base = workloads.scaled(base, args.size)
     # weak scaling: the same recipe (box side fixed) on N_lat ~ N_1 * M^(1/3),
-    # a multiple of M, so every GPU holds ~N_1^3 sites (M=1: the config itself)
-    n_lat = weak_n(base.N, world)
+    # a multiple of M, so every GPU holds ~N_1^3 sites (M=1: the config itself).
+    # Strong scaling (C5, the north star's 2048^3 sharded run): the lattice
+    # itself split into M slabs; inputs only ever exist in HBM (no e2e leg)
+    strong = strong_scaling(args)
+    n_lat = base.N if strong else weak_n(base.N, world)
     w = base if n_lat == base.N else workloads.scaled(base, n_lat)
     spec = w.spec
     n = spec.N
     part = partition(spec, world)
     lo, hi = part.x_range(rank)
-    slab = Slab(spec, w=part.W, x_lo=lo, device=local)
+    slab = Slab(spec, w=part.W, x_lo=lo, device=local, single_buffer=False)
     # start field and potential generated on the device (bitwise the host
     # recipes: Philox plane stream, Coulomb floor)
     workloads.fill_slab(slab, w)
@@ -580,6 +594,29 @@ def run_dist(args):
     value = n ** 3 * args.steps / (ms * 1e-3) / 1e9
     peak, peak_kind = hbm_peak()
     slab.close()
+    if strong:
+        if rank == 0:
+            print(json.dumps({
+                "metric": "fp64 FDTD lattice-site updates/s (GLUPS)", "value": value,
+                "unit": "GLUPS", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": w.name, "N": n, "measure_every": m, "norm_every": m,
+                           "parallelism": f"z-slabs x{world} of {part.W} planes (NCCL halos "
+                                          "overlapped, exact all-reduce of plane sums)",
+                           "inputs": "device-generated per slab (workloads.fill_slab)",
+                           "l2": "inputs larger than L2; no flush"},
+                "roofline": {"bound": "hbm", "achieved": 12 * n ** 3 * args.steps /
+                             (ms * 1e-3) / 1e9 / world, "peak": peak, "unit": "GB/s",
+                             "frac": 12 * n ** 3 * args.steps / (ms * 1e-3) / 1e9 / world / peak,
+                             "traffic": None, "per": "GPU, whole timed run, 12 B per site-update",
+                             "peak_source": peak_kind},
+                "clocks": clk.summary(), "e2e": None,
+                "e2e_note": "inputs generated in HBM (no host arrays at this size)",
+                "gpu_launches": int(launches.item()), "cpu_baseline": None}), flush=True)
+        release_comms()
+        dist.destroy_process_group()
+        return
 
     # ---- e2e: the public multi-GPU API from host arrays (rank 0 holds psi0) ----
     ext = n + 2
@@ -658,6 +695,8 @@ def main():
                     help="one GPU, single-buffer slab, device-generated inputs (default for C5)")
     ap.add_argument("--size", type=int, default=0, help="rescale the config's lattice (with --single-buffer)")
     ap.add_argument("--chunk", type=int, default=0, help="planes per chunk launch of a single-buffer slab")
+    ap.add_argument("--strong", action="store_true",
+                    help="multi-GPU: split the config's lattice itself (default for C5)")
     ap.add_argument("--dist", action="store_true",
                     help="use the torch.distributed slab engine even for one rank (testing)")
     args = ap.parse_args()
@@ -665,10 +704,11 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         return run_reference(args)
-    if int(os.environ.get("WORLD_SIZE", "1")) > 1 or args.dist:
-        return run_dist(args)
-    if args.single_buffer or args.config == "C5":
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if (args.single_buffer or args.config == "C5") and world == 1 and not args.dist:
         return run_large(args)
+    if world > 1 or args.dist:
+        return run_dist(args)
     return run_single(args)
 
 

@@ -169,6 +169,10 @@ int psg_create_ex(int device, int64_t n, int64_t w, int64_t x_lo, double a, doub
                   unsigned flags, int64_t chunk, psg_slab** out);
 int psg_destroy(psg_slab* s);
 
+/* Device memory a new slab can use: free bytes plus the bytes the slabs'
+ * memory pool holds unused; total = the device's memory. */
+int psg_mem_info(int device, int64_t* avail, int64_t* total);
+
 /* Device bytes held by the slab's psi buffers and V (fields only). */
 int64_t psg_field_bytes(psg_slab* s);
 

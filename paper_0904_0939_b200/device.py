@@ -61,11 +61,34 @@ def pinned_empty(shape) -> np.ndarray:
     return np.asarray(_PinnedBlock(n)).view(np.float64).reshape(shape)
 
 
+def mem_info(device: int = 0):
+    """(available, total) device bytes for new slabs (psg_mem_info)."""
+    lib = _lib.load()
+    avail, total = ctypes.c_int64(), ctypes.c_int64()
+    check(lib.psg_mem_info(device, ctypes.byref(avail), ctypes.byref(total)))
+    return avail.value, total.value
+
+
+def slab_field_bytes(n: int, w: int, single_buffer: bool = False, chunk: int = 0) -> int:
+    """Device bytes of a slab's psi buffers and V (psg_field_bytes before
+    allocation): planes of (n+2) rows x pitch doubles, pitch = round_up(n+5, 4)."""
+    plane = (n + 2) * (((n + 5) + 3) // 4 * 4) * 8
+    if single_buffer:
+        c = min(chunk, w) if chunk > 0 else max(1, (w + 7) // 8)
+        return ((w + 4) + c + 2 + (w + 2)) * plane
+    return (2 * (w + 4) + (w + 2)) * plane
+
+
+def fits_two_buffers(n: int, w: int, device: int = 0, margin: float = 0.97) -> bool:
+    avail, _ = mem_info(device)
+    return slab_field_bytes(n, w) <= margin * avail
+
+
 class Slab:
     """One GPU's slab of local planes 0..w+1 (global x_lo-1 .. x_lo+w)."""
 
     def __init__(self, spec: LatticeSpec, w: int | None = None, x_lo: int = 1, device: int = 0,
-                 single_buffer: bool = False, chunk: int = 0):
+                 single_buffer: bool | None = None, chunk: int = 0):
         lib = _lib.load()
         if lib.psg_device_count() <= 0:
             raise DeviceError("no CUDA device visible: the hot path has no CPU fallback")
@@ -76,7 +99,10 @@ class Slab:
         self.device = device
         h = ctypes.c_void_p()
         # single_buffer: both psi buffers in one allocation, shifted by chunk + 2
-        # planes (psg_create_ex, include/psigpu.h); whole lattice only
+        # planes (psg_create_ex, include/psigpu.h); whole lattice only.  None:
+        # only when two buffers would not fit the device's available memory
+        if single_buffer is None:
+            single_buffer = self.w == self.n and not fits_two_buffers(self.n, self.w, device)
         self.single_buffer = bool(single_buffer)
         flags = 1 if self.single_buffer else 0
         check(lib.psg_create_ex(device, self.n, self.w, self.x_lo, spec.a, spec.m, spec.dtau,

@@ -579,7 +579,7 @@ def _make_slabs_local(grid, part, initial, seed, initial_file=None):
     slabs = []
     for r in range(part.M):
         lo, hi = part.x_range(r)
-        s = Slab(spec, w=part.W, x_lo=lo, device=r % ndev)
+        s = Slab(spec, w=part.W, x_lo=lo, device=r % ndev, single_buffer=False)
         s.load_grid(grid)
         if initial_file is not None:
             load_slab_planes(s, initial_file)
@@ -655,7 +655,7 @@ def evolve_parallel(grid: PotentialGrid, *, workers: int, initial: Field3D | Non
             import torch
 
             dev = torch.cuda.current_device()
-            slab = Slab(spec, w=part.W, x_lo=lo, device=dev)
+            slab = Slab(spec, w=part.W, x_lo=lo, device=dev, single_buffer=False)
         else:
             slab = slab_factory(spec, part.W, lo, r)
         slab.load_grid(grid)

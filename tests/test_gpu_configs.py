@@ -174,7 +174,8 @@ def test_c5_2048_single_gpu(gpu_lib):
     n = spec.N
     k = 4
     samples = [1, 3, 1024, n - 1]
-    with Slab(spec, single_buffer=True) as s:
+    with Slab(spec) as s:
+        assert s.single_buffer   # chosen automatically: two buffers need 207 GB
         workloads.fill_slab(s, w)
         wins = []
         for p in samples:

@@ -236,17 +236,22 @@ def test_fused_norm_partials_equal_standalone(gpu_lib, n):
     assert np.array_equal(fused, alone)
 
 
-@pytest.mark.parametrize("n,widths,steps,every,t2", [
-    (10, (2, 3, 5), 41, 10, True),
-    (40, (13, 14, 13), 61, 20, True),
-    (40, (20, 20), 60, 0, True),
-    (100, (34, 33, 33), 45, 20, True),
-    (100, (50, 50), 30, 10, False),
+@pytest.mark.parametrize("n,widths,steps,every,t2,maxp", [
+    (10, (2, 3, 5), 41, 10, True, 0),
+    (40, (13, 14, 13), 61, 20, True, 0),
+    (40, (20, 20), 60, 0, True, 0),
+    (100, (34, 33, 33), 45, 20, True, 0),
+    (100, (50, 50), 30, 10, False, 0),
+    (40, (20, 20), 60, 0, True, 3),
+    (100, (34, 33, 33), 45, 20, True, 7),
+    (100, (50, 50), 31, 10, True, 1),
 ])
-def test_multi_slab_run_matches_whole_lattice(gpu_lib, n, widths, steps, every, t2):
+def test_multi_slab_run_matches_whole_lattice(gpu_lib, n, widths, steps, every, t2, maxp):
     """psg_run_multi (slabs tiling the lattice, halos by peer copies, two-sweep
     passes with two halo planes per face) gives the bits of the whole-lattice
-    run: field, check sums and the measured observables."""
+    run: field, check sums and the measured observables.  maxp > 0 caps the
+    planes per two-sweep launch (option 9: the signalled pass of a slab beyond
+    2^32 elements, edge chunks first)."""
     from paper_0904_0939_b200.device import measure_multi, run_multi
 
     spec = LatticeSpec(N=n, a=0.3, m=1.0, dtau=0.3 * 0.3 / 4.0)
@@ -269,6 +274,7 @@ def test_multi_slab_run_matches_whole_lattice(gpu_lib, n, widths, steps, every, 
         for w in widths:
             s = Slab(spec, w=w, x_lo=lo)
             s.set_temporal(t2)
+            s.set_option(9, maxp)
             s.set_field(psi0[lo - 1:lo + w + 1])
             s.set_potential(v[lo - 1:lo + w + 1])
             slabs.append(s)

@@ -10,7 +10,7 @@ plane sums, parity imposition, device-generated inputs and resampling.
 import numpy as np
 import pytest
 
-from paper_0904_0939_b200.device import F_MEASURE, F_NORM, F_WRITE, Slab
+from paper_0904_0939_b200.device import F_MEASURE, F_NORM, F_WRITE, Slab, slab_field_bytes
 from paper_0904_0939_b200.errors import ConfigError
 from paper_0904_0939_b200.lattice import LatticeSpec
 
@@ -137,6 +137,9 @@ def test_single_buffer_memory_and_limits(gpu_lib):
         ps = one.plane_stride * 8
         assert two.field_bytes == (2 * (n + 4) + (n + 2)) * ps
         assert one.field_bytes == ((n + 4) + 10 + (n + 2)) * ps
+        assert two.field_bytes == slab_field_bytes(n, n)
+        assert one.field_bytes == slab_field_bytes(n, n, True, 8)
+        assert not two.single_buffer and one.single_buffer    # auto: two buffers fit
         with pytest.raises(ConfigError):
             one.sweep(1, n // 2, F_WRITE)       # chunk order needs the whole sweep
         with pytest.raises(ConfigError):
