@@ -394,7 +394,12 @@ int psg_tune(psg_slab* s, int blocks_per_sm, int zchunk, int stages);
  * chunk items, 2 one contiguous (tile, plane) range per block (bitwise
  * unchanged), 9 = at most this many planes per two-sweep launch (0 = as
  * many as 32-bit output offsets allow, the default; slabs beyond that are
- * passed in several launches; bitwise unchanged). */
+ * passed in several launches; bitwise unchanged), 11 = fused halo exchange of
+ * in-process slabs (psg_run_multi, read from the first slab; default 1): each
+ * two-sweep pass also stores its edge output planes into the neighbouring
+ * slabs' halo planes through peer memory (NVLink between GPUs) instead of a
+ * separate copy; needs W >= 4 and peer access, else the copies are used
+ * (bitwise unchanged). */
 int psg_set_option(psg_slab* s, int option, int value);
 
 /* Enable / disable two sweeps per HBM pass (temporal blocking) for pairs of
@@ -408,6 +413,10 @@ int psg_set_march(psg_slab* s, int enable);
 
 /* Number of kernels this slab has launched so far. */
 int64_t psg_launch_count(psg_slab* s);
+
+/* Two-sweep passes of this slab that delivered its edge planes to the
+ * neighbouring slabs by peer stores (option 11). */
+int64_t psg_fused_pass_count(psg_slab* s);
 
 #ifdef __cplusplus
 }

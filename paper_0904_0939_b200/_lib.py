@@ -121,6 +121,7 @@ SIGNATURES = {
     "psg_axpy": (c_int, [c_void_p, c_void_p, c_double]),
     "psg_copy_plane": (c_int, [c_void_p, c_int, c_int64, c_void_p, c_int, c_int64]),
     "psg_launch_count": (c_int64, [c_void_p]),
+    "psg_fused_pass_count": (c_int64, [c_void_p]),
     "psg_set_march": (c_int, [c_void_p, c_int]),
     "psg_set_temporal": (c_int, [c_void_p, c_int]),
     "psg_set_option": (c_int, [c_void_p, c_int, c_int]),

@@ -269,8 +269,10 @@ __device__ __forceinline__ bool t2b_ring_interior(const T2Item& I, int n, int x_
 }
 
 
-// one work item of an E-row warp (MASK: item touches the lattice boundary)
-template <int S, int TB, bool STEP2, bool FASTC, bool MASK>
+// one work item of an E-row warp (MASK: item touches the lattice boundary;
+// PEER: the slab's edge output planes are also stored into the neighbour
+// slabs' halo planes, peer memory over NVLink -- the fused halo exchange)
+template <int S, int TB, bool STEP2, bool FASTC, bool MASK, bool PEER = false>
 __device__ __forceinline__ void t2b_rows_item(const SweepArgs& args, const T2Item& I,
                                               uint32_t fb, uint32_t base, int w, int lane,
                                               StageRot<S, T2BGeo<TB>::STAGE>& nx, uint32_t& g) {
@@ -356,6 +358,17 @@ __device__ __forceinline__ void t2b_rows_item(const SweepArgs& args, const T2Ite
       } else if (ok0) {
         *dst = o0;
       }
+      if (PEER) {
+        const int z = p - 1;   // the output plane (uniform across the block)
+        const long long dd = z <= args.pl_hi ? args.dl : (z >= args.pr_lo ? args.dr : 0);
+        if (dd != 0) {
+          if (!MASK || ok1) {
+            *reinterpret_cast<double2*>(dst + dd) = make_double2(o0, o1);
+          } else if (ok0) {
+            dst[dd] = o0;
+          }
+        }
+      }
     }
     if (STEP2) doff += pstride;
     rg.next(rf0);
@@ -380,7 +393,7 @@ __device__ __forceinline__ void t2b_rows_item(const SweepArgs& args, const T2Ite
   }
 }
 
-template <int S, int TB, bool STEP2, bool FASTC>
+template <int S, int TB, bool STEP2, bool FASTC, bool PEER = false>
 __device__ __forceinline__ void t2b_rows(const SweepArgs& args, uint32_t sm0, int w, int lane) {
   using C = T2BCfg<S, TB>;
   const uint32_t fb = sm0 + C::BAR_OFF;               // full[S], empty[S], rfull[4]
@@ -389,9 +402,9 @@ __device__ __forceinline__ void t2b_rows(const SweepArgs& args, uint32_t sm0, in
   uint32_t g = 4;   // ring plane counter (runs across items; 0..3 are the pre-completed phases)
   t2b_for_items<TB>(args, [&](const T2Item& I) {
     if (t2b_row_interior(I, w, args.n, args.x_off))
-      t2b_rows_item<S, TB, STEP2, FASTC, false>(args, I, fb, base, w, lane, nx, g);
+      t2b_rows_item<S, TB, STEP2, FASTC, false, PEER>(args, I, fb, base, w, lane, nx, g);
     else
-      t2b_rows_item<S, TB, STEP2, FASTC, true>(args, I, fb, base, w, lane, nx, g);
+      t2b_rows_item<S, TB, STEP2, FASTC, true, PEER>(args, I, fb, base, w, lane, nx, g);
   });
 }
 
@@ -482,7 +495,7 @@ __device__ __forceinline__ void t2b_ringw(const SweepArgs& args, uint32_t sm0, i
   });
 }
 
-template <int NST, int TB, bool FASTC>
+template <int NST, int TB, bool FASTC, bool PEER = false>
 __global__ void __launch_bounds__(T2BGeo<TB>::THREADS, T2BGeo<TB>::MINB)
     k_sweep2b(const __grid_constant__ CUtensorMap tm_psi, const __grid_constant__ CUtensorMap tm_v,
               const SweepArgs args) {
@@ -540,7 +553,7 @@ __global__ void __launch_bounds__(T2BGeo<TB>::THREADS, T2BGeo<TB>::MINB)
   } else if (warp == 0 || warp == TB + 1) {
     t2b_rows<S, TB, false, FASTC>(args, sm0, warp, lane);
   } else {
-    t2b_rows<S, TB, true, FASTC>(args, sm0, warp, lane);
+    t2b_rows<S, TB, true, FASTC, PEER>(args, sm0, warp, lane);
   }
 }
 

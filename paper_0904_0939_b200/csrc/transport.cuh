@@ -26,6 +26,11 @@ struct Transport {
   virtual int post_signal(int depth) = 0;
   virtual int wait() = 0;
   virtual int allreduce() = 0;
+  // fused exchange: two-sweep passes store their edge planes straight into the
+  // neighbours' output-buffer halos (peer memory); after_fused() then orders
+  // every slab's next work after its neighbours' passes (via wait())
+  virtual bool fused() const { return false; }
+  virtual int after_fused() { return PSG_OK; }
 };
 
 struct NcclTransport : Transport {
@@ -118,10 +123,41 @@ struct LocalTransport : Transport {
     }
     CU_TRY(cudaSetDevice(sl[0]->device));
     CU_TRY(cudaMalloc(&tmp0, (size_t)NQ * sl[0]->n * sizeof(double)));
+    // fused exchange: every slab wide enough that no output plane goes both
+    // ways (W >= 4), and neighbours on one device or with peer access
+    fused_ok = m >= 2 && sl[0]->fused_halo;
+    for (int r = 0; r < m && fused_ok; ++r) fused_ok = sl[r]->w >= 4;
+    for (int r = 1; r < m && fused_ok; ++r) {
+      const int d0 = sl[r - 1]->device, d1 = sl[r]->device;
+      if (d0 == d1) continue;
+      int a01 = 0, a10 = 0;
+      CU_TRY(cudaDeviceCanAccessPeer(&a01, d0, d1));
+      CU_TRY(cudaDeviceCanAccessPeer(&a10, d1, d0));
+      if (!a01 || !a10) {
+        fused_ok = false;
+        break;
+      }
+      for (int pair = 0; pair < 2; ++pair) {
+        CU_TRY(cudaSetDevice(pair ? d1 : d0));
+        const cudaError_t e = cudaDeviceEnablePeerAccess(pair ? d0 : d1, 0);
+        if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+        else if (e != cudaSuccess) return fail(PSG_ERR_CUDA, "peer access between slab devices");
+      }
+    }
     return PSG_OK;
   }
   bool has_left(size_t r) const override { return r > 0; }
   bool has_right(size_t r) const override { return r + 1 < sl.size(); }
+  bool fused_ok = false;
+  bool fused() const override { return fused_ok; }
+  int after_fused() override {
+    for (size_t r = 0; r < sl.size(); ++r) {
+      CU_TRY(cudaSetDevice(sl[r]->device));
+      CU_TRY(cudaEventRecord(evc[r], sl[r]->stream));
+    }
+    pushed = true;   // wait(): my halos were written by my neighbours' passes
+    return PSG_OK;
+  }
   bool pushed = false;   // last exchange pushed by the source slabs (post_signal)
   int post(int depth) override {
     const size_t m = sl.size();
@@ -283,6 +319,37 @@ int multi_sweep2(std::vector<psg_slab*>& sl, Transport* tr) {
   if (rc) return rc;
   rc = tr->wait();
   if (rc) return rc;
+  if (tr->fused()) {
+    // one launch per slab computes both sweeps AND delivers its new edge planes
+    // into the neighbours' halos: a site of output plane z <= 2 is stored at
+    // the same (j, k) of the left neighbour's plane W_L + z, z >= W - 1 at the
+    // right neighbour's plane z - W (element offsets between the buffers)
+    for (size_t r = 0; r < sl.size(); ++r) {
+      psg_slab* s = sl[r];
+      CU_TRY(cudaSetDevice(s->device));
+      const long long ps = s->plane_stride;
+      const double* out = s->psi[1 - s->cur];
+      PeerStores pst;
+      if (r > 0) {
+        const psg_slab* o = sl[r - 1];
+        pst.dl = (long long)((intptr_t)(o->psi[1 - o->cur] + o->w * ps) - (intptr_t)out) / 8;
+        pst.pl_hi = 2;
+      }
+      if (r + 1 < sl.size()) {
+        const psg_slab* o = sl[r + 1];
+        pst.dr = (long long)((intptr_t)(o->psi[1 - o->cur] - s->w * ps) - (intptr_t)out) / 8;
+        pst.pr_lo = (int)s->w - 1;
+      }
+      rc = pass2(s, 1, s->w, false, &pst);
+      if (rc) return rc;
+      s->fused_passes++;
+    }
+    rc = tr->after_fused();
+    if (rc) return rc;
+    tr->deep = true;
+    for (psg_slab* s : sl) s->cur = 1 - s->cur;
+    return PSG_OK;
+  }
   for (psg_slab* s : sl) {
     CU_TRY(cudaSetDevice(s->device));
     if (!s->sig_dev) {

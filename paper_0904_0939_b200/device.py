@@ -151,6 +151,11 @@ class Slab:
     def launches(self) -> int:
         return int(self._lib.psg_launch_count(self._h))
 
+    def fused_passes(self) -> int:
+        """Two-sweep passes that stored this slab's edge planes into its
+        neighbours' halos (fused exchange, psg_run_multi)."""
+        return int(self._lib.psg_fused_pass_count(self._h))
+
     def tune(self, blocks_per_sm: int = 0, zchunk: int = 0, stages: int = 0):
         check(self._lib.psg_tune(self._h, blocks_per_sm, zchunk, stages))
 

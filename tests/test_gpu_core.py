@@ -236,22 +236,29 @@ def test_fused_norm_partials_equal_standalone(gpu_lib, n):
     assert np.array_equal(fused, alone)
 
 
-@pytest.mark.parametrize("n,widths,steps,every,t2,maxp", [
-    (10, (2, 3, 5), 41, 10, True, 0),
-    (40, (13, 14, 13), 61, 20, True, 0),
-    (40, (20, 20), 60, 0, True, 0),
-    (100, (34, 33, 33), 45, 20, True, 0),
-    (100, (50, 50), 30, 10, False, 0),
-    (40, (20, 20), 60, 0, True, 3),
-    (100, (34, 33, 33), 45, 20, True, 7),
-    (100, (50, 50), 31, 10, True, 1),
+@pytest.mark.parametrize("n,widths,steps,every,t2,maxp,fused", [
+    (10, (2, 3, 5), 41, 10, True, 0, 1),
+    (40, (13, 14, 13), 61, 20, True, 0, 1),
+    (40, (20, 20), 60, 0, True, 0, 1),
+    (100, (34, 33, 33), 45, 20, True, 0, 1),
+    (100, (50, 50), 30, 10, False, 0, 1),
+    (40, (20, 20), 60, 0, True, 3, 1),
+    (100, (34, 33, 33), 45, 20, True, 7, 1),
+    (100, (50, 50), 31, 10, True, 1, 1),
+    (40, (13, 14, 13), 61, 20, True, 0, 0),
+    (100, (34, 33, 33), 45, 20, True, 7, 0),
+    (100, (4, 30, 4, 62), 40, 10, True, 0, 1),
+    (130, (40, 50, 40), 53, 0, True, 0, 1),
 ])
-def test_multi_slab_run_matches_whole_lattice(gpu_lib, n, widths, steps, every, t2, maxp):
-    """psg_run_multi (slabs tiling the lattice, halos by peer copies, two-sweep
-    passes with two halo planes per face) gives the bits of the whole-lattice
-    run: field, check sums and the measured observables.  maxp > 0 caps the
-    planes per two-sweep launch (option 9: the signalled pass of a slab beyond
-    2^32 elements, edge chunks first)."""
+def test_multi_slab_run_matches_whole_lattice(gpu_lib, n, widths, steps, every, t2, maxp, fused):
+    """psg_run_multi (slabs tiling the lattice, two-sweep passes with two halo
+    planes per face) gives the bits of the whole-lattice run: field, check sums
+    and the measured observables.  fused = 1 (default, slabs of W >= 4): each
+    two-sweep pass stores its edge planes straight into the neighbours' halos
+    (k_sweep2b<PEER>); fused = 0: the pass signals its edge items and the
+    copy engines push the planes.  maxp > 0 caps the planes per two-sweep
+    launch (option 9: slabs beyond 2^32 elements, edge chunks first when
+    signalled)."""
     from paper_0904_0939_b200.device import measure_multi, run_multi
 
     spec = LatticeSpec(N=n, a=0.3, m=1.0, dtau=0.3 * 0.3 / 4.0)
@@ -275,6 +282,7 @@ def test_multi_slab_run_matches_whole_lattice(gpu_lib, n, widths, steps, every, 
             s = Slab(spec, w=w, x_lo=lo)
             s.set_temporal(t2)
             s.set_option(9, maxp)
+            s.set_option(11, fused)
             s.set_field(psi0[lo - 1:lo + w + 1])
             s.set_potential(v[lo - 1:lo + w + 1])
             slabs.append(s)
@@ -286,6 +294,11 @@ def test_multi_slab_run_matches_whole_lattice(gpu_lib, n, widths, steps, every, 
         meas_m = measure_multi(slabs)
         if t2 and steps > 4:
             assert sum(s.launches() for s in slabs) > 0
+            nf = [s.fused_passes() for s in slabs]
+            if fused and min(widths) >= 4 and every:   # every = 0: norm each step, no pairs
+                assert min(nf) > 0
+            else:
+                assert max(nf) == 0
     finally:
         for s in slabs:
             s.close()
