@@ -411,6 +411,12 @@ int psg_set_temporal(psg_slab* s, int enable);
  * plain steps inside psg_run (cooperative launch, per-tile dataflow flags). */
 int psg_set_march(psg_slab* s, int enable);
 
+/* One two-sweep pass (k_sweep2b) over the slab's planes with the halos it
+ * holds, then the buffer swap -- no exchange, no reductions; the pending
+ * factor must be 1.  reserve_sms: SMs left idle (a distributed run leaves 8
+ * to NCCL).  For timing a slab's pass on one GPU and for tests. */
+int psg_pass(psg_slab* s, int reserve_sms);
+
 /* Number of kernels this slab has launched so far. */
 int64_t psg_launch_count(psg_slab* s);
 

@@ -122,6 +122,7 @@ SIGNATURES = {
     "psg_copy_plane": (c_int, [c_void_p, c_int, c_int64, c_void_p, c_int, c_int64]),
     "psg_launch_count": (c_int64, [c_void_p]),
     "psg_fused_pass_count": (c_int64, [c_void_p]),
+    "psg_pass": (c_int, [c_void_p, c_int]),
     "psg_set_march": (c_int, [c_void_p, c_int]),
     "psg_set_temporal": (c_int, [c_void_p, c_int]),
     "psg_set_option": (c_int, [c_void_p, c_int, c_int]),

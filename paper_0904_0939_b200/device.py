@@ -151,6 +151,11 @@ class Slab:
     def launches(self) -> int:
         return int(self._lib.psg_launch_count(self._h))
 
+    def pass2(self, reserve_sms: int = 0):
+        """One two-sweep pass over the slab's planes with its current halos,
+        then swap (psg_pass; timing / tests)."""
+        check(self._lib.psg_pass(self._h, int(reserve_sms)))
+
     def fused_passes(self) -> int:
         """Two-sweep passes that stored this slab's edge planes into its
         neighbours' halos (fused exchange, psg_run_multi)."""

@@ -160,3 +160,24 @@ def test_two_step_pass_in_several_launches(gpu_lib, n, planes):
     assert np.array_equal(ref[0], got[0])
     assert np.array_equal(ref[1], got[1])
     assert got[3] > ref[3]
+
+
+def test_pass_entry_point_equals_run(gpu_lib):
+    """psg_pass (one two-sweep pass with the slab's halos, the timing entry of
+    scripts/slab_pass_tune.py) equals run(2) with no reductions."""
+    n = 100
+    spec = LatticeSpec(N=n, a=0.3, m=1.0, dtau=0.3 * 0.3 / 4.0)
+    psi0, v = _inputs(n, 9)
+    out = []
+    for via_pass in (False, True):
+        with Slab(spec, single_buffer=False) as s:
+            s.set_temporal(True)
+            s.set_field(psi0)
+            s.set_potential(v)
+            for _ in range(3):
+                if via_pass:
+                    s.pass2(0)
+                else:
+                    s.run(2, 0, 0)
+            out.append(s.get_field())
+    assert np.array_equal(out[0], out[1])
