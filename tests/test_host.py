@@ -244,3 +244,20 @@ def test_symmetry_tokens():
         SymmetryConstraint.from_token("Qz")
     with pytest.raises(ConfigError):
         SymmetryConstraint("w", "symmetric")
+
+
+def test_slab_field_bytes_c5_sizes():
+    """The memory arithmetic behind the single-buffer choice (device.Slab):
+    2048^3 needs 207 GB with two psi buffers (more than a B200's 183 GB) and
+    147 GB with one allocation shifted by chunk + 2 planes."""
+    from paper_0904_0939_b200.device import slab_field_bytes
+
+    plane = 2050 * 2056 * 8
+    assert slab_field_bytes(2048, 2048) == (2 * 2052 + 2050) * plane
+    assert slab_field_bytes(2048, 2048) > 183e9 * 1.1
+    one = slab_field_bytes(2048, 2048, single_buffer=True)
+    assert one == (2052 + 256 + 2 + 2050) * plane
+    assert 140e9 < one < 150e9
+    assert slab_field_bytes(64, 64, True, 8) == ((64 + 4) + 10 + 66) * 66 * 72 * 8
+    # 2 GPUs at 2048^3: three fields of a 1024-plane slab
+    assert slab_field_bytes(2048, 1024) < 110e9
