@@ -165,6 +165,9 @@ int psg_create(int device, int64_t n, int64_t w, int64_t x_lo, double a, double 
  * persistent march.  Extends evolve.SweepBuffers (evolve.py:160-166), whose
  * two full buffers are the reference's memory layout. */
 #define PSG_CREATE_SINGLE_BUFFER 1u
+/* PSG_CREATE_IPC: psi buffers from cudaMalloc, exportable to the neighbouring
+ * ranks' processes (psg_ipc_create). */
+#define PSG_CREATE_IPC 2u
 int psg_create_ex(int device, int64_t n, int64_t w, int64_t x_lo, double a, double m, double dtau,
                   unsigned flags, int64_t chunk, psg_slab** out);
 int psg_destroy(psg_slab* s);
@@ -416,6 +419,30 @@ int psg_set_march(psg_slab* s, int enable);
  * factor must be 1.  reserve_sms: SMs left idle (a distributed run leaves 8
  * to NCCL).  For timing a slab's pass on one GPU and for tests. */
 int psg_pass(psg_slab* s, int reserve_sms);
+
+/* NCCL-free slab transport between processes (one slab per process, one GPU
+ * per process, GPUs with peer access; the replacement for parallel.py's
+ * socket transport, parallel.py:179-255).  Two-sweep passes store their edge
+ * planes straight into the neighbours' halo planes (peer memory, the fused
+ * exchange); single sweeps pull the neighbours' edge planes; plane sums are
+ * all-reduced through mailboxes in every rank's memory, summed in rank order
+ * (exact, bitwise M-invariant); ordering by device counters that each rank's
+ * stream waits on (cuStreamWaitValue64) -- no kernel waits for another rank.
+ * Protocol: every rank psg_ipc_create()s (slab from PSG_CREATE_IPC) and
+ * shares its PSG_IPC_HANDLE_BYTES handle; every rank gets all handles in rank
+ * order and psg_ipc_connect()s; a host barrier; then psg_run_ipc /
+ * psg_measure_ipc in lock step (same parameters on every rank); a host
+ * barrier before psg_ipc_destroy. */
+#define PSG_IPC_HANDLE_BYTES 256
+typedef struct psg_ipc psg_ipc;
+int psg_ipc_create(psg_slab* s, int rank, int nranks, void* handle_out, psg_ipc** out);
+int psg_ipc_connect(psg_ipc* c, const void* all_handles);
+int psg_ipc_destroy(psg_ipc* c);
+int psg_run_ipc(psg_slab* s, psg_ipc* c, const psg_run_params* p, double* hist,
+                int64_t max_checks, int64_t* n_checks);
+int psg_measure_ipc(psg_slab* s, psg_ipc* c, double* rec);
+/* Halo planes this slab's IPC runs delivered to its neighbours. */
+int64_t psg_ipc_halo_planes(psg_slab* s);
 
 /* Number of kernels this slab has launched so far. */
 int64_t psg_launch_count(psg_slab* s);

@@ -111,6 +111,12 @@ SIGNATURES = {
     "psg_run_dist": (c_int, [c_void_p, c_void_p, c_int, c_int, POINTER(RunParams), _dp, c_int64,
                              _lp]),
     "psg_measure_dist": (c_int, [c_void_p, c_void_p, c_int, c_int, _dp]),
+    "psg_ipc_create": (c_int, [c_void_p, c_int, c_int, c_void_p, POINTER(c_void_p)]),
+    "psg_ipc_connect": (c_int, [c_void_p, c_void_p]),
+    "psg_ipc_destroy": (c_int, [c_void_p]),
+    "psg_run_ipc": (c_int, [c_void_p, c_void_p, POINTER(RunParams), _dp, c_int64, _lp]),
+    "psg_measure_ipc": (c_int, [c_void_p, c_void_p, _dp]),
+    "psg_ipc_halo_planes": (c_int64, [c_void_p]),
     "psg_run_multi": (c_int, [POINTER(c_void_p), c_int, POINTER(RunParams), _dp, c_int64, _lp]),
     "psg_measure_multi": (c_int, [POINTER(c_void_p), c_int, _dp]),
     "psg_tune": (c_int, [c_void_p, c_int, c_int, c_int]),

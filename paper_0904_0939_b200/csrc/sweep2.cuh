@@ -406,6 +406,9 @@ __device__ __forceinline__ void t2b_rows(const SweepArgs& args, uint32_t sm0, in
     else
       t2b_rows_item<S, TB, STEP2, FASTC, true, PEER>(args, I, fb, base, w, lane, nx, g);
   });
+  // peer stores performed system-wide before the kernel completes (another
+  // GPU learns of them from a counter written after this launch)
+  if (PEER && STEP2) __threadfence_system();
 }
 
 template <int S, int TB, bool FASTC, bool MASK>

@@ -31,6 +31,12 @@ struct Transport {
   // every slab's next work after its neighbours' passes (via wait())
   virtual bool fused() const { return false; }
   virtual int after_fused() { return PSG_OK; }
+  // slab r's neighbour on `side` (0 left, 1 right): its OUTPUT buffer of the
+  // pass about to run (local plane 0) and its W; nullptr when there is none
+  virtual double* peer_out(size_t r, int side, int64_t* w) const {
+    (void)r; (void)side; (void)w;
+    return nullptr;
+  }
 };
 
 struct NcclTransport : Transport {
@@ -150,6 +156,12 @@ struct LocalTransport : Transport {
   bool has_right(size_t r) const override { return r + 1 < sl.size(); }
   bool fused_ok = false;
   bool fused() const override { return fused_ok; }
+  double* peer_out(size_t r, int side, int64_t* w) const override {
+    const size_t q = side ? r + 1 : r - 1;
+    if ((side == 0 && r == 0) || q >= sl.size()) return nullptr;
+    *w = sl[q]->w;
+    return sl[q]->psi[1 - sl[q]->cur];
+  }
   int after_fused() override {
     for (size_t r = 0; r < sl.size(); ++r) {
       CU_TRY(cudaSetDevice(sl[r]->device));
@@ -330,14 +342,13 @@ int multi_sweep2(std::vector<psg_slab*>& sl, Transport* tr) {
       const long long ps = s->plane_stride;
       const double* out = s->psi[1 - s->cur];
       PeerStores pst;
-      if (r > 0) {
-        const psg_slab* o = sl[r - 1];
-        pst.dl = (long long)((intptr_t)(o->psi[1 - o->cur] + o->w * ps) - (intptr_t)out) / 8;
+      int64_t wl = 0, wr = 0;
+      if (const double* lo = tr->peer_out(r, 0, &wl)) {
+        pst.dl = (long long)((intptr_t)(lo + wl * ps) - (intptr_t)out) / 8;
         pst.pl_hi = 2;
       }
-      if (r + 1 < sl.size()) {
-        const psg_slab* o = sl[r + 1];
-        pst.dr = (long long)((intptr_t)(o->psi[1 - o->cur] - s->w * ps) - (intptr_t)out) / 8;
+      if (const double* ro = tr->peer_out(r, 1, &wr)) {
+        pst.dr = (long long)((intptr_t)(ro - s->w * ps) - (intptr_t)out) / 8;
         pst.pr_lo = (int)s->w - 1;
       }
       rc = pass2(s, 1, s->w, false, &pst);

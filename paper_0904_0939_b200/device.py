@@ -88,7 +88,7 @@ class Slab:
     """One GPU's slab of local planes 0..w+1 (global x_lo-1 .. x_lo+w)."""
 
     def __init__(self, spec: LatticeSpec, w: int | None = None, x_lo: int = 1, device: int = 0,
-                 single_buffer: bool | None = None, chunk: int = 0):
+                 single_buffer: bool | None = None, chunk: int = 0, ipc: bool = False):
         lib = _lib.load()
         if lib.psg_device_count() <= 0:
             raise DeviceError("no CUDA device visible: the hot path has no CPU fallback")
@@ -102,9 +102,11 @@ class Slab:
         # planes (psg_create_ex, include/psigpu.h); whole lattice only.  None:
         # only when two buffers would not fit the device's available memory
         if single_buffer is None:
-            single_buffer = self.w == self.n and not fits_two_buffers(self.n, self.w, device)
+            single_buffer = (self.w == self.n and not ipc
+                             and not fits_two_buffers(self.n, self.w, device))
         self.single_buffer = bool(single_buffer)
-        flags = 1 if self.single_buffer else 0
+        # ipc: psi buffers other processes can map (IpcLink, the NCCL-free transport)
+        flags = (1 if self.single_buffer else 0) | (2 if ipc else 0)
         check(lib.psg_create_ex(device, self.n, self.w, self.x_lo, spec.a, spec.m, spec.dtau,
                                 flags, int(chunk), ctypes.byref(h)))
         self._h = h
@@ -462,6 +464,10 @@ class Slab:
         p, max_checks, hist = self._run_params(steps, measure_every, norm_every, reimpose_every,
                                                constraints, step_offset, max_checks)
         nc = ctypes.c_int64()
+        if isinstance(comm, IpcLink):   # NCCL-free: neighbours from the link's handles
+            check(self._lib.psg_run_ipc(self._h, comm.handle, ctypes.byref(p), dptr(hist),
+                                        max_checks, ctypes.byref(nc)))
+            return self._unpack_hist(hist, nc.value)
         check(self._lib.psg_run_dist(self._h, comm.handle, -1 if left is None else int(left),
                                      -1 if right is None else int(right), ctypes.byref(p),
                                      dptr(hist), max_checks, ctypes.byref(nc)))
@@ -471,6 +477,9 @@ class Slab:
         """Plane sums (3, N) of the current state of a slab of a z-decomposed
         lattice, all-reduced over the ranks (psg_measure_dist)."""
         rec = np.zeros(3 * self.n + 2)
+        if isinstance(comm, IpcLink):
+            check(self._lib.psg_measure_ipc(self._h, comm.handle, dptr(rec)))
+            return rec[2:].reshape(3, self.n)
         check(self._lib.psg_measure_dist(self._h, comm.handle, -1 if left is None else int(left),
                                          -1 if right is None else int(right), dptr(rec)))
         return rec[2:].reshape(3, self.n)
@@ -567,3 +576,54 @@ class Comm:
             self.close()
         except Exception:
             pass
+
+
+IPC_HANDLE_BYTES = 256
+
+
+class IpcLink:
+    """NCCL-free transport of one slab per process (psg_ipc_*): the slab's
+    two-sweep passes store their edge planes into the neighbours' halos through
+    CUDA IPC mappings of their buffers, plane sums are all-reduced through
+    mailboxes, ordering by device counters.  Used like Comm by
+    Slab.run_dist / measure_dist.  Every rank must construct it (slab created
+    with ipc=True), exchange ``handle`` in rank order (``connect``), and pass a
+    host barrier before the first run and before ``close``."""
+
+    def __init__(self, slab: "Slab", rank: int, world: int):
+        self._lib = _lib.load()
+        self.slab = slab
+        self.rank, self.world = rank, world
+        buf = ctypes.create_string_buffer(IPC_HANDLE_BYTES)
+        h = ctypes.c_void_p()
+        check(self._lib.psg_ipc_create(slab.handle, rank, world, buf, ctypes.byref(h)))
+        self.handle = h
+        self.export = buf.raw
+
+    def connect(self, handles):
+        if len(handles) != self.world or any(len(b) != IPC_HANDLE_BYTES for b in handles):
+            raise ConfigError("one IPC handle per rank expected")
+        blob = ctypes.create_string_buffer(b"".join(handles), IPC_HANDLE_BYTES * self.world)
+        check(self._lib.psg_ipc_connect(self.handle, blob))
+
+    @classmethod
+    def from_process_group(cls, slab: "Slab"):
+        """Create, exchange handles over the default torch process group (any
+        backend), connect, barrier."""
+        import torch.distributed as dist
+
+        rank, world = dist.get_rank(), dist.get_world_size()
+        link = cls(slab, rank, world)
+        allh = [None] * world
+        dist.all_gather_object(allh, link.export)
+        link.connect(allh)
+        dist.barrier()
+        return link
+
+    def halo_messages(self) -> int:
+        return int(self._lib.psg_ipc_halo_planes(self.slab.handle))
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self._lib.psg_ipc_destroy(self.handle)
+            self.handle = None
