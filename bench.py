@@ -559,9 +559,15 @@ def run_dist(args):
 
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
-    local = int(os.environ.get("LOCAL_RANK", rank))
+    # one GPU per rank (the modulo only matters for protocol runs that share a GPU)
+    local = int(os.environ.get("LOCAL_RANK", rank)) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    ipc = args.transport == "ipc"
+    if ipc:   # the IPC transport needs torch.distributed only for the host handshake
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    coll_dev = "cpu" if ipc else "cuda"
     base = workload(args.config)
     if args.size:
         base = workloads.scaled(base, args.size)
@@ -576,7 +582,7 @@ def run_dist(args):
     n = spec.N
     part = partition(spec, world)
     lo, hi = part.x_range(rank)
-    slab = Slab(spec, w=part.W, x_lo=lo, device=local, single_buffer=False)
+    slab = Slab(spec, w=part.W, x_lo=lo, device=local, single_buffer=False, ipc=ipc)
     # start field and potential generated on the device (bitwise the host
     # recipes: Philox plane stream, Coulomb floor)
     workloads.fill_slab(slab, w)
@@ -588,7 +594,12 @@ def run_dist(args):
     grid.spec = spec
     grid.unbounded = w.potential in ("cornell", "wells")
     grid.v_inf = 0.0
-    comm = get_comm(local)   # cached: the e2e calls below reuse it
+    if ipc:   # NCCL-free: halos stored by the sweep kernel through CUDA IPC mappings
+        from paper_0904_0939_b200.device import IpcLink
+
+        comm = IpcLink.from_process_group(slab)
+    else:
+        comm = get_comm(local)   # cached: the e2e calls below reuse it
     engine = SlabEngine(grid, part, [slab], [rank], _DistGroup(slab, rank, part, comm))
     m = w.measure_every
     kw = dict(tol=1e-300, check_freq=m, snap_freq=10 ** 12, reimpose_freq=10 ** 12,
@@ -607,13 +618,16 @@ def run_dist(args):
         e1.synchronize()
         torch.cuda.synchronize()
         dist.barrier()
-    ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+    ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=coll_dev)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    launches = torch.tensor([float(slab.launches() - l0)], dtype=torch.float64, device="cuda")
+    launches = torch.tensor([float(slab.launches() - l0)], dtype=torch.float64, device=coll_dev)
     dist.all_reduce(launches)
     ms = float(ms.item())
     value = n ** 3 * args.steps / (ms * 1e-3) / 1e9
     peak, peak_kind = hbm_peak()
+    if ipc:
+        dist.barrier()
+        comm.close()
     slab.close()
     if strong:
         if rank == 0:
@@ -623,8 +637,10 @@ def run_dist(args):
                 "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": w.name, "N": n, "measure_every": m, "norm_every": m,
-                           "parallelism": f"z-slabs x{world} of {part.W} planes (NCCL halos "
-                                          "overlapped, exact all-reduce of plane sums)",
+                           "parallelism": f"z-slabs x{world} of {part.W} planes ("
+                                          + ("IPC: halos stored by the sweep kernel"
+                                             if ipc else "NCCL halos overlapped")
+                                          + ", exact all-reduce of plane sums)",
                            "inputs": "device-generated per slab (workloads.fill_slab)",
                            "l2": "inputs larger than L2; no flush"},
                 "roofline": {"bound": "hbm", "achieved": 12 * n ** 3 * args.steps /
@@ -656,10 +672,10 @@ def run_dist(args):
         dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        st_e = evolve_parallel(pgrid, workers=world, initial=init, transport="nccl",
+        st_e = evolve_parallel(pgrid, workers=world, initial=init, transport=args.transport,
                                scatter_initial=True, check_freq=m, max_steps=args.steps,
                                max_snapshots=0, norm_every=m, fixed=True)
-        dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+        dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=coll_dev)
         dist.all_reduce(dt, op=dist.ReduceOp.MAX)
         if i >= E2E_WARMUP:
             e2e_times.append(float(dt.item()))
@@ -674,8 +690,12 @@ def run_dist(args):
                        "weak": f"{base.name} recipe (box side {base.N * base.a:g}) on N = the "
                                f"multiple of lcm(64, M) nearest {base.N}*M^(1/3): "
                                f"{n ** 3 / world / 1e6:.2f} M sites per GPU",
-                       "parallelism": f"z-slabs x{world} (NCCL: two halo planes per face every "
-                                      f"other sweep, overlapped; exact all-reduce of plane sums)",
+                       "transport": args.transport,
+                       "parallelism": f"z-slabs x{world} (" + (
+                           "IPC: two halo planes per face stored by each two-sweep pass into "
+                           "the neighbours' buffers" if ipc else
+                           "NCCL: two halo planes per face every other sweep, overlapped")
+                       + "; exact all-reduce of plane sums)",
                        "l2": "inputs larger than L2; no flush"},
             # whole timed run per GPU: a two-sweep pass moves 24 B per site for two
             # updates (12 B per site-update); the few single sweeps around the
@@ -716,6 +736,9 @@ def main():
                     help="one GPU, single-buffer slab, device-generated inputs (default for C5)")
     ap.add_argument("--size", type=int, default=0, help="rescale the config's lattice (with --single-buffer)")
     ap.add_argument("--chunk", type=int, default=0, help="planes per chunk launch of a single-buffer slab")
+    ap.add_argument("--transport", choices=["nccl", "ipc"], default="nccl",
+                    help="multi-GPU slab transport: NCCL (device-triggered exchange) or the "
+                         "NCCL-free IPC transport (halos stored by the sweep kernel)")
     ap.add_argument("--strong", action="store_true",
                     help="multi-GPU: split the config's lattice itself (default for C5)")
     ap.add_argument("--dist", action="store_true",

@@ -432,7 +432,9 @@ class SlabEngine:
             import torch
 
             t = torch.tensor([float(self.halo_messages + comm.halo_messages() - h0)],
-                             dtype=torch.float64, device=s.torch_device())
+                             dtype=torch.float64,
+                             device=s.torch_device() if self.group.dist.get_backend() == "nccl"
+                             else "cpu")
             self.group.dist.all_reduce(t)
             self.halo_messages = int(t.item())
         return final, checks, snaps, converged, step_count, started
@@ -461,7 +463,9 @@ class SlabEngine:
             planes = s.get_field(1, s.w)
             import torch
 
-            mine = torch.from_numpy(np.ascontiguousarray(planes)).to(s.torch_device())
+            mine = torch.from_numpy(np.ascontiguousarray(planes))
+            if self.group.dist.get_backend() == "nccl":
+                mine = mine.to(s.torch_device())
             theirs = torch.empty_like(mine)
             if mirror == rank:
                 theirs.copy_(mine)
@@ -504,7 +508,8 @@ class SlabEngine:
             s = self.slabs[0]
             dist = self.group.dist
             rank = self.ranks[0]
-            if not s.torch_device().type == "cuda":   # CPU test slabs over gloo
+            if s.torch_device().type != "cuda" or dist.get_backend() != "nccl":
+                # CPU test slabs, or GPU slabs whose group is gloo (IPC transport)
                 mine = torch.from_numpy(np.ascontiguousarray(s.get_field(1, s.w)))
                 if rank == 0:
                     parts = [mine] + [torch.empty_like(mine) for _ in range(self.part.M - 1)]
@@ -625,7 +630,9 @@ def evolve_parallel(grid: PotentialGrid, *, workers: int, initial: Field3D | Non
     ``transport="inproc"`` drives all slabs from this process and returns
     the state; ``"nccl"``/``"tcp"`` runs this process's rank of an
     initialised torch.distributed group (rank 0 returns the state, others
-    None).  ``slab_factory(spec, w, x_lo, rank)`` overrides the slab type
+    None); ``"ipc"`` is the same with the NCCL-free native transport (halos
+    stored by the sweep kernel into the neighbours' buffers through CUDA IPC,
+    device-counter ordering; any process-group backend).  ``slab_factory(spec, w, x_lo, rank)`` overrides the slab type
     (tests use it to run the protocol on CPU slabs over gloo).
     """
     spec = grid.spec
@@ -641,7 +648,7 @@ def evolve_parallel(grid: PotentialGrid, *, workers: int, initial: Field3D | Non
     if transport == "inproc":
         slabs = _make_slabs_local(grid, part, initial, seed, initial_file)
         engine = SlabEngine(grid, part, slabs, list(range(workers)), _LocalGroup(slabs, native))
-    elif transport in ("nccl", "tcp", "dist"):
+    elif transport in ("nccl", "tcp", "dist", "ipc"):
         import torch.distributed as dist
 
         if not dist.is_initialized():
@@ -655,7 +662,8 @@ def evolve_parallel(grid: PotentialGrid, *, workers: int, initial: Field3D | Non
             import torch
 
             dev = torch.cuda.current_device()
-            slab = Slab(spec, w=part.W, x_lo=lo, device=dev, single_buffer=False)
+            slab = Slab(spec, w=part.W, x_lo=lo, device=dev, single_buffer=False,
+                        ipc=transport == "ipc")
         else:
             slab = slab_factory(spec, part.W, lo, r)
         slab.load_grid(grid)
@@ -668,7 +676,12 @@ def evolve_parallel(grid: PotentialGrid, *, workers: int, initial: Field3D | Non
         else:
             slab.set_field(_initial_planes(spec, initial, seed, lo, hi), 0)
         comm = None
-        if slab_factory is None and native and dist.get_backend() == "nccl":
+        if slab_factory is None and transport == "ipc":
+            # NCCL-free: peer memory of the neighbours' slabs (any process-group backend)
+            from .device import IpcLink
+
+            comm = IpcLink.from_process_group(slab)
+        elif slab_factory is None and native and dist.get_backend() == "nccl":
             comm = get_comm(slab.device)
         engine = SlabEngine(grid, part, [slab], [r], _DistGroup(slab, r, part, comm))
     else:
@@ -688,6 +701,12 @@ def evolve_parallel(grid: PotentialGrid, *, workers: int, initial: Field3D | Non
             else:
                 save_wavefunction_slabs(engine.slabs, checkpoint_path, step_count)
     finally:
+        from .device import IpcLink
+
+        link = getattr(engine.group, "comm", None)
+        if isinstance(link, IpcLink):
+            engine.group.dist.barrier()   # no rank still writes into this slab
+            link.close()
         for s in engine.slabs:
             s.close()
     if final is None and (gather or not (isinstance(engine.group, _LocalGroup)
@@ -722,6 +741,20 @@ def _scatter_initial(slab, part, rank, initial, spec):
         t[:, :, -1] = 0.0
         return t
 
+    if dist.get_backend() != "nccl":   # gloo group (IPC transport): host buffers
+        if rank == 0:
+            for dst in range(part.M):
+                lo, hi = part.x_range(dst)
+                t = shell(torch.from_numpy(np.array(initial.values[lo - 1:hi + 2])))
+                if dst == 0:
+                    slab.set_field(t.numpy(), 0)
+                else:
+                    dist.send(t, dst)
+        else:
+            t = torch.empty((w + 2, ext, ext), dtype=torch.float64)
+            dist.recv(t, 0)
+            slab.set_field(t.numpy(), 0)
+        return None
     buf = torch.empty((w + 2, ext, ext), dtype=torch.float64, device=dev)
     if rank == 0:
         for dst in range(part.M):

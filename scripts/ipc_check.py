@@ -32,6 +32,8 @@ def main():
     ap.add_argument("--steps", type=int, default=61)
     ap.add_argument("--every", type=int, default=20)
     ap.add_argument("--device", type=int, default=-1, help="-1: LOCAL_RANK modulo visible GPUs")
+    ap.add_argument("--api", action="store_true",
+                    help="through evolve_parallel(transport='ipc') against workers=1 (inproc)")
     a = ap.parse_args()
     dist.init_process_group("gloo")
     rank, world = dist.get_rank(), dist.get_world_size()
@@ -47,6 +49,8 @@ def main():
     v = np.zeros((ext,) * 3)
     v[1:-1, 1:-1, 1:-1] = rng.uniform(-1.0, 3.0, (n, n, n))
     every = a.every
+    if a.api:
+        return api_check(a, spec, psi0, v, rank, world)
     with Slab(spec, device=dev, single_buffer=False) as whole:
         whole.set_temporal(True)
         whole.set_field(psi0)
@@ -84,6 +88,37 @@ def main():
     print(f"IPC_OK rank={rank} fused={fused}", flush=True)
     dist.destroy_process_group()
     return 0
+
+
+def api_check(a, spec, psi0, v, rank, world):
+    """evolve_parallel(transport="ipc") from rank 0's host field (scattered
+    over the gloo group), a converging run with checks and snapshots and a
+    fixed run, against the single-slab engine: same fields and checks."""
+    from paper_0904_0939_b200 import Field3D, evolve_parallel
+    from paper_0904_0939_b200.potential import custom
+
+    n = spec.N
+    grid = custom(spec, v[1:-1, 1:-1, 1:-1], v_inf=0.0, unbounded=False)
+    init = Field3D(spec, psi0)
+    ok = True
+    for kw in (dict(tol=1e-300, check_freq=a.every or 10, max_steps=a.steps, max_snapshots=2,
+                    snap_freq=2 * (a.every or 10)),
+               dict(check_freq=a.every or 10, max_steps=a.steps, max_snapshots=0, fixed=True,
+                    norm_every=a.every or 10)):
+        got = evolve_parallel(grid, workers=world, initial=init if rank == 0 else None,
+                              transport="ipc", scatter_initial=True, **kw)
+        if rank == 0:
+            want = evolve_parallel(grid, workers=1, initial=init, transport="inproc", **kw)
+            ok = ok and np.array_equal(got.psi.values, want.psi.values)
+            ok = ok and [c.energy for c in got.checks] == [c.energy for c in want.checks]
+            ok = ok and len(got.snapshots) == len(want.snapshots) and all(
+                np.array_equal(x[1].values, y[1].values) for x, y in zip(got.snapshots,
+                                                                         want.snapshots))
+        else:
+            ok = ok and got is None
+    print(("IPC_OK" if ok else "IPC_FAIL") + f" rank={rank} fused=1", flush=True)
+    dist.destroy_process_group()
+    return 0 if ok else 1
 
 
 if __name__ == "__main__":

@@ -35,3 +35,18 @@ def test_ipc_transport_bitwise(gpu_lib, ranks, n, steps, every):
         r.stdout[-2000:] + r.stderr[-3000:]
     if every:   # plain pairs ran as fused two-sweep passes
         assert all(int(f) > 0 for _, f in ok)
+
+
+@pytest.mark.parametrize("ranks,n,steps,every", [(2, 40, 60, 10), (4, 64, 41, 10)])
+def test_ipc_evolve_parallel_api(gpu_lib, ranks, n, steps, every):
+    """evolve_parallel(transport="ipc"): scatter from rank 0, converging run
+    with checks and snapshots, fixed run; equal to the one-slab engine."""
+    port = 29700 + 10 * ranks + n % 10
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={ranks}", "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.join(ROOT, "scripts", "ipc_check.py"), "--lattice", str(n), "--steps",
+           str(steps), "--every", str(every), "--api"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT)
+    ok = re.findall(r"IPC_OK rank=(\d+)", r.stdout)
+    assert r.returncode == 0 and sorted(int(x) for x in ok) == list(range(ranks)), \
+        r.stdout[-2000:] + r.stderr[-3000:]
