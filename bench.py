@@ -11,13 +11,14 @@ second (GLUPS), whole job.  psi (2 buffers) + V are 3 x 137 MB, larger than
 the 126 MB L2, so no flush is needed between steps.
 
 JSON fields beyond the base contract:
-  roofline      dominant kernel vs measured HBM copy bandwidth.  For N >= 96
+  roofline      dominant kernel vs measured HBM copy bandwidth.  For N >= 8
                 the run's plain steps go in pairs through k_sweep2b (two
                 sweeps per HBM pass): one launch reads psi and V and writes
                 psi once for 2 N^3 site-updates, so achieved = 24 B/site x
                 N^3 / mean launch duration (CUDA events on the slab's stream);
-                below N = 96 the kernel is k_sweep (one sweep per launch, same
-                24 B/site).  traffic from the committed ncu capture (profiles/).
+                with temporal blocking off the kernel is k_sweep (one sweep per
+                launch, same 24 B/site).  traffic from the committed ncu capture
+                (profiles/).
   cpu_baseline  the CPU oracle port (oracle/, C + OpenMP, all host threads) on
                 a bounded sample of the same workload, rank 0, N=1.
   e2e           the same metric through the public API (evolve_fixed) from

@@ -406,7 +406,7 @@ int psg_tune(psg_slab* s, int blocks_per_sm, int zchunk, int stages);
 int psg_set_option(psg_slab* s, int option, int value);
 
 /* Enable / disable two sweeps per HBM pass (temporal blocking) for pairs of
- * plain steps inside psg_run; default on for N >= 288 (measured crossover);
+ * plain steps inside psg_run; default on for N >= 8 (faster at every size measured);
  * results are bitwise unchanged. */
 int psg_set_temporal(psg_slab* s, int enable);
 

@@ -205,7 +205,7 @@ class Slab:
         self.set_option(3, rows)
 
     def set_temporal(self, enable: bool):
-        """Two sweeps per HBM pass for pairs of plain steps in run() (default: N >= 96)."""
+        """Two sweeps per HBM pass for pairs of plain steps in run() (default: N >= 8)."""
         check(self._lib.psg_set_temporal(self._h, 1 if enable else 0))
 
     def set_zchunk(self, zc: int):

@@ -309,7 +309,7 @@ def evolve_to_convergence(initial: Field3D, grid: PotentialGrid, tol: float = 1e
     and snapshots see a normalised state; k = check_freq is BASELINE's cadence).  The update is linear, so this changes the iterate only
     by roundoff (~1e-16 relative; SURVEY 8(c) measured 6.6e-16 after 2000
     steps at k = 100) while letting pairs of plain sweeps run as one two-sweep
-    pass over HBM (~2x faster from N = 96 on).
+    pass over HBM (faster at every size measured).
     """
     from .device import Slab
 
