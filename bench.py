@@ -55,6 +55,20 @@ PEAK_FALLBACK = 6650.0  # GB/s, B200_PROFILING.md fallback when MEASURED_PEAKS.j
 BYTES_PER_SITE = 24     # psi read + V read + psi write, fp64
 
 
+def cpu_model() -> str:
+    """The host CPU's model name and logical CPU count (lscpu's "Model name")."""
+    name = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    name = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return f"{name} ({os.cpu_count()} logical CPUs)"
+
+
 def hbm_peak():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -246,6 +260,7 @@ def run_reference(args):
                    "measure_every": w.measure_every},
         "impl": "reference",
         "cpu_baseline": {"value": glups, "unit": "GLUPS", "cores": O.threads(), "kind": "port",
+                         "cpu": cpu_model(),
                          "sample": sample},
         "e2e": {"value": glups, "unit": "GLUPS", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
@@ -383,7 +398,8 @@ def run_single(args):
     cpu = None
     if not args.no_cpu:
         g, cores, sample = cpu_sample(w)
-        cpu = {"value": g, "unit": "GLUPS", "cores": cores, "kind": "port", "sample": sample}
+        cpu = {"value": g, "unit": "GLUPS", "cores": cores, "kind": "port", "sample": sample,
+               "cpu": cpu_model()}
 
     line = {
         "metric": "fp64 FDTD lattice-site updates/s (GLUPS)",
