@@ -580,11 +580,15 @@ def run_dist(args):
     local = int(os.environ.get("LOCAL_RANK", rank)) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     ipc = args.transport == "ipc"
-    if ipc:   # the IPC transport needs torch.distributed only for the host handshake
+    # the IPC transport needs torch.distributed only for the handshake and the
+    # e2e leg's scatter / gather: NCCL when every rank has its own GPU, gloo
+    # when ranks share one (protocol runs on a one-GPU box)
+    shared = world > torch.cuda.device_count()
+    if ipc and shared:
         dist.init_process_group("gloo")
     else:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    coll_dev = "cpu" if ipc else "cuda"
+    coll_dev = "cpu" if (ipc and shared) else "cuda"
     base = workload(args.config)
     if args.size:
         base = workloads.scaled(base, args.size)
