@@ -400,15 +400,30 @@ __device__ __forceinline__ void t2b_rows(const SweepArgs& args, uint32_t sm0, in
   const uint32_t base = sm0 + (uint32_t)(((w + 1) * BOXW + 2 * lane + 2) * 8);
   StageRot<S, T2BGeo<TB>::STAGE> nx(base, fb);
   uint32_t g = 4;   // ring plane counter (runs across items; 0..3 are the pre-completed phases)
-  t2b_for_items<TB>(args, [&](const T2Item& I) {
-    if (t2b_row_interior(I, w, args.n, args.x_off))
-      t2b_rows_item<S, TB, STEP2, FASTC, false, PEER>(args, I, fb, base, w, lane, nx, g);
-    else
-      t2b_rows_item<S, TB, STEP2, FASTC, true, PEER>(args, I, fb, base, w, lane, nx, g);
-  });
-  // peer stores performed system-wide before the kernel completes (another
-  // GPU learns of them from a counter written after this launch)
-  if (PEER && STEP2) __threadfence_system();
+  if constexpr (PEER && STEP2) {
+    t2b_for_items<TB>(args, [&](const T2Item& I) {
+      // only items holding an edge output plane take the peer-store variant
+      const bool edge = I.z0 <= args.pl_hi || I.z1 >= args.pr_lo;
+      if (t2b_row_interior(I, w, args.n, args.x_off)) {
+        if (edge) t2b_rows_item<S, TB, STEP2, FASTC, false, true>(args, I, fb, base, w, lane, nx, g);
+        else t2b_rows_item<S, TB, STEP2, FASTC, false, false>(args, I, fb, base, w, lane, nx, g);
+      } else {
+        if (edge) t2b_rows_item<S, TB, STEP2, FASTC, true, true>(args, I, fb, base, w, lane, nx, g);
+        else t2b_rows_item<S, TB, STEP2, FASTC, true, false>(args, I, fb, base, w, lane, nx, g);
+      }
+    });
+    // no fence here: the peer stores are performed when this grid completes;
+    // whoever reads them is ordered after that completion (an event, or the
+    // IPC transport's post kernel, which fences at system scope and then
+    // publishes its counter)
+  } else {
+    t2b_for_items<TB>(args, [&](const T2Item& I) {
+      if (t2b_row_interior(I, w, args.n, args.x_off))
+        t2b_rows_item<S, TB, STEP2, FASTC, false>(args, I, fb, base, w, lane, nx, g);
+      else
+        t2b_rows_item<S, TB, STEP2, FASTC, true>(args, I, fb, base, w, lane, nx, g);
+    });
+  }
 }
 
 template <int S, int TB, bool FASTC, bool MASK>
