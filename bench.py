@@ -579,6 +579,11 @@ def run_dist(args):
     # one GPU per rank (the modulo only matters for protocol runs that share a GPU)
     local = int(os.environ.get("LOCAL_RANK", rank)) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
+    if args.transport == "auto":
+        ndev = torch.cuda.device_count()
+        peers = all(torch.cuda.can_device_access_peer(i, j)
+                    for i in range(ndev) for j in range(ndev) if i != j)
+        args.transport = "ipc" if (world > 1 and world <= ndev and peers) else "nccl"
     ipc = args.transport == "ipc"
     # the IPC transport needs torch.distributed only for the handshake and the
     # e2e leg's scatter / gather: NCCL when every rank has its own GPU, gloo
@@ -731,7 +736,7 @@ def run_dist(args):
                     "h2d_bytes_per_step": 2 * ext ** 3 * 8 / args.steps,
                     "d2h_bytes_per_step": (ext ** 3 * 8 + len(st_e.checks) * (3 * n + 2) * 8)
                     / args.steps,
-                    "api": "paper_0904_0939_b200.evolve_parallel(transport='nccl', "
+                    "api": f"paper_0904_0939_b200.evolve_parallel(transport='{args.transport}', "
                            "scatter_initial=True, fixed=True) from host arrays on rank 0 (psi0) "
                            "and every rank (V); psi gathered to rank 0 inside the timed region",
                     "calls_s": [round(t, 4) for t in e2e_times],
@@ -757,9 +762,10 @@ def main():
                     help="one GPU, single-buffer slab, device-generated inputs (default for C5)")
     ap.add_argument("--size", type=int, default=0, help="rescale the config's lattice (with --single-buffer)")
     ap.add_argument("--chunk", type=int, default=0, help="planes per chunk launch of a single-buffer slab")
-    ap.add_argument("--transport", choices=["nccl", "ipc"], default="nccl",
+    ap.add_argument("--transport", choices=["auto", "nccl", "ipc"], default="auto",
                     help="multi-GPU slab transport: NCCL (device-triggered exchange) or the "
-                         "NCCL-free IPC transport (halos stored by the sweep kernel)")
+                         "NCCL-free IPC transport (halos stored by the sweep kernel); auto = "
+                         "IPC when every pair of local GPUs has peer access, else NCCL")
     ap.add_argument("--strong", action="store_true",
                     help="multi-GPU: split the config's lattice itself (default for C5)")
     ap.add_argument("--dist", action="store_true",

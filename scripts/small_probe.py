@@ -1,8 +1,9 @@
 """Per-sweep time of the fused loop at small lattices (developer tool): two-sweep
-passes on / off, CUDA-graph capture (option 12) on / off, renormalisation
-every 100 sweeps (BASELINE) or every sweep (psibox's evolve_to_convergence).
+passes on / off, renormalisation every 100 sweeps (BASELINE) or every sweep
+(psibox's evolve_to_convergence).  (A CUDA-graph capture option was measured
+here and removed: DESIGN.md section 8.)
 
-    python scripts/small_probe.py [--sizes 32,64,96,128,256] [--t2 0,1] [--graph 0,1]
+    python scripts/small_probe.py [--sizes 32,64,96,128,256] [--t2 0,1]
         [--norm 100,1] [--steps 2000] [--segment 0]
 
 --segment k: issue the steps as run() calls of k sweeps (the convergence
@@ -25,7 +26,6 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--sizes", default="32,64,96,128")
     ap.add_argument("--t2", default="0,1")
-    ap.add_argument("--graph", default="0")
     ap.add_argument("--norm", default="100")
     ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--segment", type=int, default=0)
@@ -34,11 +34,10 @@ def main():
         w = workloads.scaled(workloads.CONFIGS["C1"], n)
         for ne in [int(x) for x in a.norm.split(",")]:
             for t2 in [int(x) for x in a.t2.split(",")]:
-                for g in [int(x) for x in a.graph.split(",")]:
+                for g in (0,):
                     s = Slab(w.spec)
                     workloads.fill_slab(s, w)
                     s.set_temporal(bool(t2))
-                    s.set_option(12, g)
                     st = torch.cuda.ExternalStream(s.stream)
                     seg = a.segment or a.steps
                     s.run(2 * seg, 0, ne)
