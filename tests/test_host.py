@@ -261,3 +261,24 @@ def test_slab_field_bytes_c5_sizes():
     assert slab_field_bytes(64, 64, True, 8) == ((64 + 4) + 10 + 66) * 66 * 72 * 8
     # 2 GPUs at 2048^3: three fields of a 1024-plane slab
     assert slab_field_bytes(2048, 1024) < 110e9
+
+
+def test_bench_helpers():
+    """bench.py's weak-scaling sizes and its model of psg_run's pass schedule."""
+    import bench
+
+    assert bench.weak_n(256, 1) == 256
+    for m in (2, 4, 8):
+        n = bench.weak_n(256, m)
+        assert n % m == 0 and n % 64 == 0
+        assert abs(n ** 3 / m - 256 ** 3) / 256 ** 3 < 0.2
+    assert [bench.weak_n(256, m) for m in (2, 4, 8)] == [320, 384, 512]
+    # pairing rule: runs of plain steps in pairs; measure (state index % m == 0)
+    # and norm (step % m == 0) steps single
+    passes, singles = bench.t2_schedule(4000, 100, 500)
+    assert 2 * passes + singles == 4000
+    # steps 101..4100: 8 norm + 8 measure steps, and the odd plain runs
+    # 101..499 and 4002..4100 each leave one single step
+    assert singles == 18
+    passes, singles = bench.t2_schedule(10, 0, 0)
+    assert (passes, singles) == (5, 0)
