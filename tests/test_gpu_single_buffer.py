@@ -140,6 +140,10 @@ def test_single_buffer_memory_and_limits(gpu_lib):
         assert two.field_bytes == slab_field_bytes(n, n)
         assert one.field_bytes == slab_field_bytes(n, n, True, 8)
         assert not two.single_buffer and one.single_buffer    # auto: two buffers fit
+        from paper_0904_0939_b200.device import mem_info
+
+        avail, total = mem_info(0)
+        assert 0 < avail <= total and total > 100e9   # a B200's HBM
         with pytest.raises(ConfigError):
             one.sweep(1, n // 2, F_WRITE)       # chunk order needs the whole sweep
         with pytest.raises(ConfigError):
