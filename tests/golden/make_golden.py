@@ -169,8 +169,82 @@ def config1_fixture():
          plane_sums=psi.sum(axis=(1, 2)), max_abs=np.array([np.abs(psi).max()]))
 
 
+def _aniso_harmonic(spec):
+    """V = (x^2 + 2 y^2 + 3 z^2)/2 on the storage axes: no degenerate levels,
+    so the first excited state is unique (extraction is well posed)."""
+    c = (spec.N + 1) / 2.0
+    i = (np.arange(1, spec.N + 1) - c) * spec.a
+    x, y, z = np.meshgrid(i, i, i, indexing="ij")
+    return potential.custom(spec, 0.5 * (x * x + 2.0 * y * y + 3.0 * z * z))
+
+
+def next_rows_fixture():
+    """SURVEY 8(f) rows through the reference's own functions: QWF1 bytes
+    (multires.py:56-65), project_out (states.py:102-128), extract_excited
+    (states.py:140-209) and bootstrap_run (multires.py:170-254)."""
+    import tempfile
+
+    from psibox.evolve import renormalize
+
+    out = {}
+    # QWF1: the exact bytes of a wavefunction and a potential file
+    spec4 = lattice.LatticeSpec(N=4, a=0.7, m=1.5, dtau=0.7 * 0.7 / 4)
+    f4 = lattice.fill_random_gaussian(lattice.allocate(spec4), 9)
+    with tempfile.TemporaryDirectory() as d:
+        p = os.path.join(d, "w.qwf")
+        multires.write_field_file(p, f4.values, spec4, step_count=17)
+        out["qwf_psi_bytes"] = np.frombuffer(open(p, "rb").read(), dtype=np.uint8)
+        g4 = potential.harmonic(spec4)
+        multires.write_field_file(p, g4.v, spec4, v_inf=2.5, kind=multires.KIND_POTENTIAL)
+        out["qwf_pot_bytes"] = np.frombuffer(open(p, "rb").read(), dtype=np.uint8)
+    out["qwf_psi"] = f4.values
+    out["qwf_pot"] = g4.v
+
+    # project_out against a two-state orthonormal basis
+    spec8 = lattice.LatticeSpec(N=8, a=0.5, m=1.0, dtau=0.5 * 0.5 / 4)
+    b1, _ = renormalize(lattice.fill_random_gaussian(lattice.allocate(spec8), 1))
+    b2, _ = renormalize(states.project_out(
+        renormalize(lattice.fill_random_gaussian(lattice.allocate(spec8), 2))[0], [b1]))
+    snap = lattice.fill_random_gaussian(lattice.allocate(spec8), 3)
+    out["proj_b1"], out["proj_b2"], out["proj_snap"] = b1.values, b2.values, snap.values
+    out["proj_out"] = states.project_out(snap, [b1, b2]).values
+
+    # extract_excited from a converged run with snapshots
+    spec = lattice.LatticeSpec(N=8, a=0.7, m=1.0, dtau=0.7 * 0.7 / 4)
+    grid = _aniso_harmonic(spec)
+    init = lattice.fill_random_gaussian(lattice.allocate(spec), 5)
+    st = evolve_to_convergence(init, grid, tol=1e-10, check_freq=50, snap_freq=100,
+                               max_steps=30000, max_snapshots=8)
+    assert st.converged
+    (psi1, e1), = states.extract_excited(st, grid, 1, polish_steps=400, check_freq=50)
+    out["ex_init"] = init.values
+    out["ex_steps"] = np.array([st.step_count])
+    out["ex_psi0"] = st.psi.values
+    out["ex_snap_tau"] = np.array([t for t, _ in st.snapshots])
+    out["ex_snaps"] = np.stack([s.values for _, s in st.snapshots])
+    out["ex_psi1"] = psi1.values
+    out["ex_e1"] = np.array([e1, observables.energy(st.psi, grid)])
+
+    # bootstrap_run: 8^3 -> 16^3 at fixed box side, ground state carried, and a
+    # two-state carry (extract_excited between the stages)
+    ladder = [lattice.LatticeSpec(N=n, a=6.0 / n, m=1.0, dtau=(6.0 / n) ** 2 / 4.0)
+              for n in (8, 16)]
+    for tag, kw in (("g", dict(max_snapshots=0)),
+                    ("c", dict(max_snapshots=8, snap_freq=40, carry_coefficients=[1.0, 0.3],
+                               polish_steps=200))):
+        bs = multires.bootstrap_run(ladder, _aniso_harmonic, seed=4, tol=1e-8, check_freq=20,
+                                    max_steps=20000, **kw)
+        out[f"boot_{tag}_psi"] = bs.psi.values
+        out[f"boot_{tag}_iters"] = np.array([r.iterations for r in bs.stage_reports])
+        out[f"boot_{tag}_energy"] = np.array([r.energy for r in bs.stage_reports])
+    save("next_rows", **out)
+
+
 if __name__ == "__main__":
     print("reference", psibox.__version__)
+    if sys.argv[1:] == ["next_rows"]:
+        next_rows_fixture()
+        sys.exit(0)
     kernels_fixture()
     potentials_fixture()
     lattice_fixture()

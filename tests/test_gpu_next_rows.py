@@ -1,0 +1,88 @@
+"""GPU parity of SURVEY 8(f)'s rows against the reference's own outputs
+(tests/golden/next_rows.npz, made by tests/golden/make_golden.py next_rows):
+project_out (states.py:102-128), extract_excited (states.py:140-209) and
+bootstrap_run (multires.py:170-254), each through the public API on the GPU.
+
+Tolerances: these are convergence-driven runs (hundreds of sweeps with
+renormalisation and projection) on the device, whose plane sums are
+tree-ordered where the reference's are sequential; fields agree to 1e-11 of
+their maximum, energies to 1e-11 relative, and every convergence decision
+(stopping step, stage iteration counts) exactly."""
+
+import os
+
+import numpy as np
+import pytest
+
+from paper_0904_0939_b200 import LatticeSpec, custom, evolve_to_convergence, project_out
+from paper_0904_0939_b200.evolve import EvolutionState
+from paper_0904_0939_b200.lattice import Field3D
+from paper_0904_0939_b200.multires import bootstrap_run
+from paper_0904_0939_b200.observables import energy
+from paper_0904_0939_b200.states import extract_excited
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+TOL = 1e-11
+
+
+@pytest.fixture(scope="module")
+def g():
+    return np.load(os.path.join(GOLD, "next_rows.npz"))
+
+
+def aniso_harmonic(spec):
+    """Same recipe as make_golden._aniso_harmonic (no degenerate levels)."""
+    c = (spec.N + 1) / 2.0
+    i = (np.arange(1, spec.N + 1) - c) * spec.a
+    x, y, z = np.meshgrid(i, i, i, indexing="ij")
+    return custom(spec, 0.5 * (x * x + 2.0 * y * y + 3.0 * z * z))
+
+
+def close(got, want, tol=TOL):
+    return np.abs(got - want).max() <= tol * np.abs(want).max()
+
+
+def test_project_out_matches_reference(gpu_lib, g):
+    spec = LatticeSpec(N=8, a=0.5, m=1.0, dtau=0.5 * 0.5 / 4)
+    basis = [Field3D(spec, g["proj_b1"].copy()), Field3D(spec, g["proj_b2"].copy())]
+    out = project_out(Field3D(spec, g["proj_snap"].copy()), basis)
+    assert close(out.values, g["proj_out"], 1e-13)
+
+
+def test_extract_excited_matches_reference(gpu_lib, g):
+    spec = LatticeSpec(N=8, a=0.7, m=1.0, dtau=0.7 * 0.7 / 4)
+    grid = aniso_harmonic(spec)
+    # the converged run itself: same stopping step, same ground state
+    st = evolve_to_convergence(Field3D(spec, g["ex_init"].copy()), grid, tol=1e-10,
+                               check_freq=50, snap_freq=100, max_steps=30000, max_snapshots=8)
+    assert st.converged and st.step_count == int(g["ex_steps"][0])
+    assert close(st.psi.values, g["ex_psi0"])
+    assert [t for t, _ in st.snapshots] == list(g["ex_snap_tau"])
+    # extraction from the reference's own converged state and snapshots
+    ref_state = EvolutionState(
+        psi=Field3D(spec, g["ex_psi0"].copy()), tau=st.tau, step_count=st.step_count,
+        snapshots=[(t, Field3D(spec, s.copy())) for t, s in zip(g["ex_snap_tau"], g["ex_snaps"])],
+        converged=True)
+    (psi1, e1), = extract_excited(ref_state, grid, 1, polish_steps=400, check_freq=50)
+    assert close(psi1.values, g["ex_psi1"])
+    assert e1 == pytest.approx(g["ex_e1"][0], rel=TOL)
+    assert energy(ref_state.psi, grid) == pytest.approx(g["ex_e1"][1], rel=TOL)
+    # and from our own run end to end
+    (psi1b, e1b), = extract_excited(st, grid, 1, polish_steps=400, check_freq=50)
+    assert close(psi1b.values, g["ex_psi1"]) and e1b == pytest.approx(g["ex_e1"][0], rel=TOL)
+
+
+@pytest.mark.parametrize("tag,kw", [
+    ("g", dict(max_snapshots=0)),
+    ("c", dict(max_snapshots=8, snap_freq=40, carry_coefficients=[1.0, 0.3], polish_steps=200)),
+])
+def test_bootstrap_run_matches_reference(gpu_lib, g, tag, kw):
+    ladder = [LatticeSpec(N=n, a=6.0 / n, m=1.0, dtau=(6.0 / n) ** 2 / 4.0) for n in (8, 16)]
+    st = bootstrap_run(ladder, aniso_harmonic, seed=4, tol=1e-8, check_freq=20,
+                       max_steps=20000, **kw)
+    assert [r.iterations for r in st.stage_reports] == list(g[f"boot_{tag}_iters"])
+    for r, e in zip(st.stage_reports, g[f"boot_{tag}_energy"]):
+        assert r.energy == pytest.approx(e, rel=TOL)
+    assert close(st.psi.values, g[f"boot_{tag}_psi"])

@@ -282,3 +282,19 @@ def test_bench_helpers():
     assert singles == 18
     passes, singles = bench.t2_schedule(10, 0, 0)
     assert (passes, singles) == (5, 0)
+
+
+def test_qwf1_bytes_match_reference_files(tmp_path):
+    """QWF1 files written by the reference (multires.py:56-65; fixture
+    next_rows.npz) are byte-identical to ours for the same field / potential,
+    and ours read theirs back exactly."""
+    g = gold("next_rows")
+    spec = LatticeSpec(N=4, a=0.7, m=1.5, dtau=0.7 * 0.7 / 4)
+    write_field_file(tmp_path / "w.qwf", g["qwf_psi"], spec, step_count=17)
+    assert (tmp_path / "w.qwf").read_bytes() == g["qwf_psi_bytes"].tobytes()
+    write_field_file(tmp_path / "v.qwf", g["qwf_pot"], spec, v_inf=2.5, kind=1)
+    assert (tmp_path / "v.qwf").read_bytes() == g["qwf_pot_bytes"].tobytes()
+    (tmp_path / "r.qwf").write_bytes(g["qwf_pot_bytes"].tobytes())
+    vals, hdr = read_field_file(tmp_path / "r.qwf")
+    assert np.array_equal(vals, g["qwf_pot"])
+    assert (hdr.kind, hdr.N, hdr.a, hdr.m, hdr.v_inf) == (1, 4, 0.7, 1.5, 2.5)
