@@ -237,6 +237,22 @@ def next_rows_fixture():
         out[f"boot_{tag}_psi"] = bs.psi.values
         out[f"boot_{tag}_iters"] = np.array([r.iterations for r in bs.stage_reports])
         out[f"boot_{tag}_energy"] = np.array([r.energy for r in bs.stage_reports])
+    # the reference's slab engine (threads): cross-slab antisymmetry along
+    # storage axis 0 (mirror exchange, parallel.py:272-323) with periodic
+    # re-imposition, run to convergence on 4 slabs
+    spec12 = lattice.LatticeSpec(N=12, a=0.5, m=1.0, dtau=0.5 * 0.5 / 4)
+    g12 = _aniso_harmonic(spec12)
+    init12 = lattice.fill_random_gaussian(lattice.allocate(spec12), 6)
+    cx = states.SymmetryConstraint("x", "antisymmetric")
+    states.impose_inplace(init12.values, spec12.N, cx)
+    par = evolve_parallel(g12, workers=4, initial=init12, tol=1e-9, check_freq=20,
+                          constraints=[cx], reimpose_freq=20, max_steps=20000,
+                          max_snapshots=0)
+    assert par.converged
+    out["par_init"] = init12.values
+    out["par_psi"] = par.psi.values
+    out["par_steps"] = np.array([par.step_count])
+    out["par_checks"] = np.array([[c.step, c.energy, c.norm2, c.r_rms] for c in par.checks])
     save("next_rows", **out)
 
 

@@ -86,3 +86,24 @@ def test_bootstrap_run_matches_reference(gpu_lib, g, tag, kw):
     for r, e in zip(st.stage_reports, g[f"boot_{tag}_energy"]):
         assert r.energy == pytest.approx(e, rel=TOL)
     assert close(st.psi.values, g[f"boot_{tag}_psi"])
+
+
+@pytest.mark.parametrize("workers", [1, 2, 4])
+def test_evolve_parallel_cross_slab_antisymmetry_matches_reference(gpu_lib, g, workers):
+    """The reference's slab engine (parallel.py:523-594, 4 thread slabs) with
+    an antisymmetry constraint along the slab axis (mirror exchange,
+    parallel.py:272-323) run to convergence, against our slab engine on 1, 2
+    and 4 in-process slabs: same stopping step and checks, same field."""
+    from paper_0904_0939_b200 import SymmetryConstraint, evolve_parallel
+
+    spec = LatticeSpec(N=12, a=0.5, m=1.0, dtau=0.5 * 0.5 / 4)
+    grid = aniso_harmonic(spec)
+    cx = SymmetryConstraint("x", "antisymmetric")
+    st = evolve_parallel(grid, workers=workers, initial=Field3D(spec, g["par_init"].copy()),
+                         tol=1e-9, check_freq=20, constraints=[cx], reimpose_freq=20,
+                         max_steps=20000, max_snapshots=0)
+    assert st.converged and st.step_count == int(g["par_steps"][0])
+    got = np.array([[c.step, c.energy, c.norm2, c.r_rms] for c in st.checks])
+    assert np.array_equal(got[:, 0], g["par_checks"][:, 0])
+    np.testing.assert_allclose(got[:, 1:], g["par_checks"][:, 1:], rtol=TOL, atol=0)
+    assert close(st.psi.values, g["par_psi"])
