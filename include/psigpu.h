@@ -176,6 +176,12 @@ int psg_destroy(psg_slab* s);
  * memory pool holds unused; total = the device's memory. */
 int psg_mem_info(int device, int64_t* avail, int64_t* total);
 
+/* Host-side singular-coefficient scan (no GPU needed): *first_bad = the first
+ * flat C-order index with 1 + h*v == 0 (h = dtau/2), or -1.  Replaces the
+ * numpy scan of potential._coefficients (potential.py:102-110) at
+ * PotentialGrid construction: multithreaded, no full-size temporaries. */
+int psg_host_find_singular(const double* v, int64_t count, double h, int64_t* first_bad);
+
 /* Device bytes held by the slab's psi buffers and V (fields only). */
 int64_t psg_field_bytes(psg_slab* s);
 

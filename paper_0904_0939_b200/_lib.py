@@ -82,6 +82,7 @@ SIGNATURES = {
     "psg_destroy": (c_int, [c_void_p]),
     "psg_field_bytes": (c_int64, [c_void_p]),
     "psg_mem_info": (c_int, [c_int, _lp, _lp]),
+    "psg_host_find_singular": (c_int, [_dp, c_int64, c_double, _lp]),
     "psg_stream": (c_void_p, [c_void_p]),
     "psg_sync": (c_int, [c_void_p]),
     "psg_geometry": (c_int, [c_void_p, _lp, _lp, _lp]),

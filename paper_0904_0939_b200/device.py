@@ -313,6 +313,8 @@ class Slab:
         c_planes = self._planes_arg(c_planes)
         check(self._lib.psg_set_coefficients(self._h, dptr(a_planes), dptr(c_planes), first,
                                              a_planes.shape[0]))
+        # A/C mode until the next V upload: a later load_grid must upload again
+        self._v_owner = None
 
     def load_grid(self, grid):
         """Upload V of a host PotentialGrid (whole lattice or this slab's part)."""

@@ -404,6 +404,11 @@ class SlabEngine:
                         raise DivergenceError("field norm diverged (check dtau against a^2/3)")
             if ax0 and done % reimpose_freq == 0:
                 self._impose(ax0, done)
+            # snapshot of the state after sweep `done` (renormalised, re-imposed)
+            # before the check on that same state decides to stop: the
+            # reference's order (parallel.py:480-485, evolve.py:266-270)
+            if done % snap_freq == 0 and len(snaps) < max_snapshots:
+                snaps.append((done * spec.dtau, self.gather()))
             started = done
             if tracker is not None and m > 0 and done == next_check and done < max_steps:
                 next_check += m
@@ -423,8 +428,6 @@ class SlabEngine:
                     converged_at = done
                     started = done + 1
                     break
-            if done % snap_freq == 0 and len(snaps) < max_snapshots:
-                snaps.append((done * spec.dtau, self.gather()))
         converged = converged_at is not None
         step_count = converged_at if converged else max_steps
         final = self.gather() if gather else None

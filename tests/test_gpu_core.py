@@ -41,6 +41,32 @@ def test_sweep_bitwise(gpu_lib, n):
     assert np.array_equal(got, want)
 
 
+def test_new_potential_clears_coefficient_mode(gpu_lib):
+    """Precomputed A/C arrays (psg_set_coefficients) are used until the next V
+    upload or fill: a slab given A/C for V1 and then V2 sweeps with V2's
+    coefficients (and load_grid uploads again after set_coefficients)."""
+    n = 24
+    spec, psi, v1 = _case(n, 501, pad=0.0)
+    _, _, v2 = _case(n, 502)
+    A1, _, C1 = O.coefficients(v1, spec.dtau, spec.m, spec.a)
+    want1 = psi.copy()
+    O.stencil_update(psi, A1, C1, want1, 1, n)
+    want2 = psi.copy()
+    O.stencil_update_v(psi, v2, spec.dtau, spec.m, spec.a, want2, 1, n)
+    with Slab(spec) as s:
+        s.set_field(psi)
+        s.set_coefficients(A1, C1)
+        s.sweep(1, n, F_WRITE)
+        s.swap()
+        assert np.array_equal(s.get_field(), want1)
+        s.set_field(psi)
+        s.set_potential(v2)
+        idx, sums, status = s.run(2, 0, 0)   # a plain pair: the two-sweep pass is allowed again
+        want22 = want2.copy()
+        O.stencil_update_v(want2, v2, spec.dtau, spec.m, spec.a, want22, 1, n)
+        assert np.array_equal(s.get_field(), want22)
+
+
 @pytest.mark.parametrize("n", [8, 33, 128])
 def test_fused_norm_and_measure(gpu_lib, n):
     spec, psi, v = _case(n, 7 + n)
