@@ -161,8 +161,7 @@ int psg_create(int device, int64_t n, int64_t w, int64_t x_lo, double a, double 
  * so no piece overwrites a plane a later piece still reads.  Results are
  * bitwise those of psg_create.  chunk = 0: ceil(w / 8).  A 2048^3 lattice
  * (psi 73.6 GB + V 69.1 GB) then fits one B200.  Not for psg_run_dist /
- * multi-slab runs (there each GPU holds a slab with its own halos) or the
- * persistent march.  Extends evolve.SweepBuffers (evolve.py:160-166), whose
+ * multi-slab runs (there each GPU holds a slab with its own halos).  Extends evolve.SweepBuffers (evolve.py:160-166), whose
  * two full buffers are the reference's memory layout. */
 #define PSG_CREATE_SINGLE_BUFFER 1u
 /* PSG_CREATE_IPC: psi buffers from cudaMalloc, exportable to the neighbouring
@@ -335,8 +334,18 @@ typedef struct psg_run_params {
   int32_t n_impose;       /* number of parity constraints (0..3), applied in order */
   int32_t impose_axis[3]; /* storage axis of each constraint */
   int32_t impose_sign[3]; /* +1 symmetric / -1 antisymmetric */
-  int32_t reserved;
+  int32_t flags;          /* PSG_RUN_* */
 } psg_run_params;
+
+/* psg_run flag: linear renormalisation pairs.  Two sweeps whose second is a
+ * renormalisation step (and whose inner state is neither measured nor
+ * re-imposed) run as one two-sweep HBM pass that applies the pending factor
+ * at the store (S(f psi) = f S(psi) up to rounding) and fuses the NORM
+ * partials of its output; the normalisation after the first sweep is
+ * subsumed by the one after the second.  evolve_to_convergence's default
+ * (renormalise every sweep, evolve.py:171-181) within roundoff, not bitwise
+ * (whole-lattice slabs; ignored by the multi-slab drivers). */
+#define PSG_RUN_LINEAR_NORM 1
 
 /* Fused fixed-step driver: runs the evolve_to_convergence loop body
  * (evolve.py:249-270) for `steps` sweeps without host round trips.
@@ -397,8 +406,7 @@ int psg_tune(psg_slab* s, int blocks_per_sm, int zchunk, int stages);
  * 3 = tile rows of the two-sweep pass, 8 (two blocks per SM) or 16 (one
  * block per SM, default; bitwise unchanged), 4 = always take the range-checked
  * coefficient path, 5 = TMA stages of the 16-row two-sweep pass (6 or 9),
- * 6 = two-sweep passes alternate their chunk order (default 1), 7 = two tile
- * rows per warp in the 16-row two-sweep pass (k_sweep2p; bitwise unchanged),
+ * 6 = two-sweep passes alternate their chunk order (default 1),
  * 8 = work split of the two-sweep pass: 0 automatic (default), 1 round-robin
  * chunk items, 2 one contiguous (tile, plane) range per block (bitwise
  * unchanged), 9 = at most this many planes per two-sweep launch (0 = as
@@ -415,10 +423,6 @@ int psg_set_option(psg_slab* s, int option, int value);
  * plain steps inside psg_run; default on for N >= 8 (faster at every size measured);
  * results are bitwise unchanged. */
 int psg_set_temporal(psg_slab* s, int enable);
-
-/* Enable / disable (default) the persistent multi-step sweep for runs of
- * plain steps inside psg_run (cooperative launch, per-tile dataflow flags). */
-int psg_set_march(psg_slab* s, int enable);
 
 /* One two-sweep pass (k_sweep2b) over the slab's planes with the halos it
  * holds, then the buffer swap -- no exchange, no reductions; the pending

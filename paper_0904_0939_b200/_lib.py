@@ -22,6 +22,7 @@ LIB_PATH = os.environ.get("PSG_LIB") or os.path.join(os.path.dirname(os.path.abs
                                                      LIB_NAME)
 
 F_WRITE = 1
+RUN_LINEAR_NORM = 1   # psg_run_params.flags: linear renormalisation pairs
 F_NORM = 2
 F_MEASURE = 4
 F_CHECK = 8
@@ -45,7 +46,7 @@ class RunParams(ctypes.Structure):
         ("n_impose", c_int32),
         ("impose_axis", c_int32 * 3),
         ("impose_sign", c_int32 * 3),
-        ("reserved", c_int32),
+        ("flags", c_int32),
     ]
 
 
@@ -130,7 +131,6 @@ SIGNATURES = {
     "psg_launch_count": (c_int64, [c_void_p]),
     "psg_fused_pass_count": (c_int64, [c_void_p]),
     "psg_pass": (c_int, [c_void_p, c_int]),
-    "psg_set_march": (c_int, [c_void_p, c_int]),
     "psg_set_temporal": (c_int, [c_void_p, c_int]),
     "psg_set_option": (c_int, [c_void_p, c_int, c_int]),
 }

@@ -44,115 +44,133 @@ __global__ void k_axpy(double* f1, const double* s1p, const double* __restrict__
     f1[i] = __dsub_rn(__dmul_rn(f1[i], s1), __dmul_rn(c, __dmul_rn(f2[i], s2)));
 }
 
-// parity: out = copy / projector of in (scaled by *sp) along `axis`, full padded extent
+// parity (states.impose_inplace, states.py:70-82, and the projector start):
+// out = copy / projector of in (scaled by *sp) along `axis`, full padded
+// extent.  One warp per row (i, j), lanes along k: every access is a
+// coalesced row segment (the mirror row too; along axis 2 it is the same row
+// read backwards), and the only integer division is one per row.
+__device__ __forceinline__ double impose_val(int ci, double self, double mir, double sign,
+                                             int mode, int first_target, int n,
+                                             bool zero_center, int center) {
+  if (mode != 0) return __dmul_rn(__dadd_rn(self, __dmul_rn(sign, mir)), 0.5);
+  if (ci >= first_target && ci <= n) return __dmul_rn(sign, mir);
+  if (zero_center && ci == center) return 0.0;
+  return self;
+}
+
 __global__ void k_impose(const double* __restrict__ in, double* __restrict__ out,
                          const double* sp, int axis, double sign, int mode, int n, int pitch,
                          long long plane_stride, int planes) {
   const int ext = n + 2;
-  const long long total = (long long)planes * ext * ext;
   const double sc = *sp;
-  const int half = n / 2;
-  const int first_target = n - half + 1;
+  const int first_target = n - n / 2 + 1;
   const bool zero_center = (n % 2 == 1) && sign < 0.0;
   const int center = (n + 1) / 2;
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
-       t += (long long)gridDim.x * blockDim.x) {
-    const int k = (int)(t % ext);
-    const long long r = t / ext;
-    const int j = (int)(r % ext);
-    const int i = (int)(r / ext);
-    int c[3] = {i, j, k};
-    const long long dst = (long long)i * plane_stride + (long long)j * pitch + k + COL_OFF;
-    const double self = __dmul_rn(in[dst], sc);
-    int m[3] = {i, j, k};
-    m[axis] = n + 1 - c[axis];
-    const long long src = (long long)m[0] * plane_stride + (long long)m[1] * pitch + m[2] + COL_OFF;
-    const double mir = __dmul_rn(in[src], sc);
-    double val;
-    if (mode == 0) {
-      const int ci = c[axis];
-      if (ci >= first_target && ci <= n) val = __dmul_rn(sign, mir);
-      else if (zero_center && ci == center) val = 0.0;
-      else val = self;
-    } else {
-      val = __dmul_rn(__dadd_rn(self, __dmul_rn(sign, mir)), 0.5);
+  const int lane = threadIdx.x & 31;
+  const int wpb = blockDim.x >> 5;
+  const int rows = planes * ext;
+  for (int row = blockIdx.x * wpb + (threadIdx.x >> 5); row < rows; row += gridDim.x * wpb) {
+    const int i = row / ext;
+    const int j = row - i * ext;
+    const long long base = (long long)i * plane_stride + (long long)j * pitch + COL_OFF;
+    long long mbase = base;   // mirror row (axes 0, 1)
+    if (axis == 0) mbase = (long long)(n + 1 - i) * plane_stride + (long long)j * pitch + COL_OFF;
+    else if (axis == 1) mbase = (long long)i * plane_stride + (long long)(n + 1 - j) * pitch + COL_OFF;
+    const int cr = axis == 0 ? i : j;   // coordinate along the axis (row-uniform unless axis 2)
+    for (int k = lane; k < ext; k += 32) {
+      const double self = __dmul_rn(in[base + k], sc);
+      const double mir = __dmul_rn(in[axis == 2 ? base + (n + 1 - k) : mbase + k], sc);
+      out[base + k] = impose_val(axis == 2 ? k : cr, self, mir, sign, mode, first_target, n,
+                                 zero_center, center);
     }
-    out[dst] = val;
   }
 }
 
-// k_impose in place (single-buffer slabs): one thread per mirror pair
-// (c, n+1-c) along `axis` reads both sites before writing either, so the
-// values are those of k_impose (same operations per site)
+// k_impose in place (single-buffer slabs): each lane owns a mirror pair
+// (c, n+1-c) along `axis` and reads both sites before writing either, so the
+// values are those of k_impose (same operations per site).  Rows as in
+// k_impose: axis 0 -> rows (c, j) for c <= (n+1)/2, lanes along k; axis 1 ->
+// rows (i, c); axis 2 -> rows (i, j), lanes along c <= (n+1)/2.
 __global__ void k_impose_pairs(double* f, const double* sp, int axis, double sign, int mode, int n,
                                int pitch, long long plane_stride) {
   const int ext = n + 2;
   const int hext = (n + 1) / 2 + 1;   // c = 0 .. (n+1)/2 (the centre pairs with itself for odd n)
-  const long long total = (long long)hext * ext * ext;
   const double sc = *sp;
-  const int half = n / 2;
-  const int first_target = n - half + 1;
+  const int first_target = n - n / 2 + 1;
   const bool zero_center = (n % 2 == 1) && sign < 0.0;
   const int center = (n + 1) / 2;
-  const long long st[3] = {plane_stride, (long long)pitch, 1};
-  auto val = [&](int ci, double self, double mir) {
-    if (mode != 0) return __dmul_rn(__dadd_rn(self, __dmul_rn(sign, mir)), 0.5);
-    if (ci >= first_target && ci <= n) return __dmul_rn(sign, mir);
-    if (zero_center && ci == center) return 0.0;
-    return self;
-  };
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
-       t += (long long)gridDim.x * blockDim.x) {
-    // t enumerates (c, u, v): c along `axis`, u, v the other two axes in order
-    const int v = (int)(t % ext);
-    const long long r = t / ext;
-    const int u = (int)(r % ext);
-    const int c = (int)(r / ext);
-    const int m = n + 1 - c;
-    int ax[3], q = 0;
-    for (int d = 0; d < 3; ++d) ax[d] = d == axis ? -1 : (q++ == 0 ? u : v);
-    long long base = COL_OFF;
-    for (int d = 0; d < 3; ++d)
-      if (d != axis) base += (long long)ax[d] * st[d];
-    const long long pc = base + (long long)c * st[axis];
-    const long long pm = base + (long long)m * st[axis];
-    const double xc = __dmul_rn(f[pc], sc);
-    const double xm = __dmul_rn(f[pm], sc);
-    f[pc] = val(c, xc, xm);
-    if (m != c) f[pm] = val(m, xm, xc);
+  const int lane = threadIdx.x & 31;
+  const int wpb = blockDim.x >> 5;
+  const int rows = axis == 2 ? ext * ext : hext * ext;
+  const int inner = axis == 2 ? hext : ext;
+  for (int row = blockIdx.x * wpb + (threadIdx.x >> 5); row < rows; row += gridDim.x * wpb) {
+    const int div = axis == 1 ? hext : ext;
+    const int r0 = row / div;            // axis 0: c; axis 1: i; axis 2: i
+    const int r1 = row - r0 * div;       // axis 0: j; axis 1: c (< hext); axis 2: j
+    for (int t = lane; t < inner; t += 32) {
+      long long pc, pm;
+      int c;
+      if (axis == 0) {
+        c = r0;
+        pc = (long long)c * plane_stride + (long long)r1 * pitch + t + COL_OFF;
+        pm = (long long)(n + 1 - c) * plane_stride + (long long)r1 * pitch + t + COL_OFF;
+      } else if (axis == 1) {
+        c = r1;
+        pc = (long long)r0 * plane_stride + (long long)c * pitch + t + COL_OFF;
+        pm = (long long)r0 * plane_stride + (long long)(n + 1 - c) * pitch + t + COL_OFF;
+      } else {
+        c = t;
+        const long long b = (long long)r0 * plane_stride + (long long)r1 * pitch + COL_OFF;
+        pc = b + c;
+        pm = b + (n + 1 - c);
+      }
+      const int m = n + 1 - c;
+      const double xc = __dmul_rn(f[pc], sc);
+      const double xm = __dmul_rn(f[pm], sc);
+      f[pc] = impose_val(c, xc, xm, sign, mode, first_target, n, zero_center, center);
+      if (m != c) f[pm] = impose_val(m, xm, xc, sign, mode, first_target, n, zero_center, center);
+    }
   }
 }
 
 // trilinear resample, bitwise replica of multires._axis_interp applied along
-// axis 0, then 1, then 2: each lerp is lo + f*(hi - lo)
+// axis 0, then 1, then 2 (multires.py:116-154): each lerp is lo + f*(hi - lo).
+// One warp per fine row (a, b), lanes along c: the fine row is written
+// coalesced; the four coarse rows (ia|ia+1, ib|ib+1) it reads are fixed per row
+// and their segments are shared by neighbouring lanes (L1).
 __global__ void k_resample(const double* __restrict__ coarse, const double* csp, int nc,
                            int cpitch, long long cplane, double* __restrict__ fine, int nf,
                            int fpitch, long long fplane, const int* __restrict__ i0,
                            const double* __restrict__ fr) {
-  const long long total = (long long)nf * nf * nf;
+  (void)nc;
   const double sc = *csp;
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
-       t += (long long)gridDim.x * blockDim.x) {
-    const int c = (int)(t % nf);
-    const long long r = t / nf;
-    const int b = (int)(r % nf);
-    const int a = (int)(r / nf);
-    const int ia = i0[a], ib = i0[b], ic = i0[c];
-    const double fa = fr[a], fb = fr[b], fc = fr[c];
-    auto at = [&](int i, int j, int k) {
-      return __dmul_rn(coarse[(long long)i * cplane + (long long)j * cpitch + k + COL_OFF], sc);
-    };
-    auto lerp = [](double lo, double hi, double f) {
-      return __dadd_rn(lo, __dmul_rn(f, __dsub_rn(hi, lo)));
-    };
-    double t1[2];
+  const int lane = threadIdx.x & 31;
+  const int wpb = blockDim.x >> 5;
+  const int rows = nf * nf;
+  auto lerp = [](double lo, double hi, double f) {
+    return __dadd_rn(lo, __dmul_rn(f, __dsub_rn(hi, lo)));
+  };
+  for (int row = blockIdx.x * wpb + (threadIdx.x >> 5); row < rows; row += gridDim.x * wpb) {
+    const int a = row / nf;
+    const int b = row - a * nf;
+    const int ia = __ldg(i0 + a), ib = __ldg(i0 + b);
+    const double fa = __ldg(fr + a), fb = __ldg(fr + b);
+    const double* r00 = coarse + (long long)ia * cplane + (long long)ib * cpitch + COL_OFF;
+    const double* r10 = r00 + cplane;
+    const double* r01 = r00 + cpitch;
+    const double* r11 = r10 + cpitch;
+    double* dst = fine + (long long)(a + 1) * fplane + (long long)(b + 1) * fpitch + 1 + COL_OFF;
+    for (int c = lane; c < nf; c += 32) {
+      const int ic = __ldg(i0 + c);
+      const double fc = __ldg(fr + c);
+      double t1[2];
 #pragma unroll
-    for (int dk = 0; dk < 2; ++dk) {
-      const double t0lo = lerp(at(ia, ib, ic + dk), at(ia + 1, ib, ic + dk), fa);
-      const double t0hi = lerp(at(ia, ib + 1, ic + dk), at(ia + 1, ib + 1, ic + dk), fa);
-      t1[dk] = lerp(t0lo, t0hi, fb);
+      for (int dk = 0; dk < 2; ++dk) {
+        const double t0lo = lerp(__dmul_rn(r00[ic + dk], sc), __dmul_rn(r10[ic + dk], sc), fa);
+        const double t0hi = lerp(__dmul_rn(r01[ic + dk], sc), __dmul_rn(r11[ic + dk], sc), fa);
+        t1[dk] = lerp(t0lo, t0hi, fb);
+      }
+      dst[c] = lerp(t1[0], t1[1], fc);
     }
-    fine[(long long)(a + 1) * fplane + (long long)(b + 1) * fpitch + (c + 1) + COL_OFF] =
-        lerp(t1[0], t1[1], fc);
   }
 }

@@ -180,13 +180,14 @@ __device__ void combine_body(const double* plane_sums, int n, unsigned qmask, do
   }
 }
 
-// tile partials -> plane sums: one warp per plane, lane l sums tiles l, l+32, ...
+// tile partials [q][plane][tiles] (q at qstride) -> plane sums: one warp per
+// plane, lane l sums tiles l, l+32, ...
 // sequentially, then the fixed xor butterfly; with `combine`, the last block to
 // finish runs the cross-plane combine
 constexpr int RED_WARPS = 8;
 __global__ void __launch_bounds__(32 * RED_WARPS)
     k_plane_reduce(const double* __restrict__ part, double* plane_sums, unsigned qmask,
-                   int planes, int tiles, int z_lo, int z_hi, int x_off, int n, int* counter,
+                   long long qstride, int tiles, int z_lo, int z_hi, int x_off, int n, int* counter,
                    int combine, double a3, double* scal, double* hist_rec, const int* bad) {
   __shared__ CombineSmem sm;
   // launched as a programmatic dependent of the sweep: wait for its partials
@@ -198,7 +199,7 @@ __global__ void __launch_bounds__(32 * RED_WARPS)
     const int gplane = x_off + p - 1;  // 0-based interior index of this plane
     for (int q = 0; q < NQ; ++q) {
       if (!(qmask & (1u << q))) continue;
-      const double* src = part + ((size_t)q * planes + p) * tiles;
+      const double* src = part + (size_t)q * qstride + (size_t)p * tiles;
       double acc = 0.0;
       for (int t = lane; t < tiles; t += 32) acc = __dadd_rn(acc, src[t]);
       acc = warp_sum(acc);

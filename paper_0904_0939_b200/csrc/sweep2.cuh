@@ -17,6 +17,20 @@
 // registers rotate by renaming, shared memory is addressed by 32-bit offsets
 // with immediates and the output pointer advances by one plane stride.
 // ------------------------------------------------------------------
+// one site of the update from explicit neighbours, the reference's order
+// (kernels.py:33-37): left-to-right sum of the six neighbours, minus 6 psi,
+// A psi + C s
+__device__ __forceinline__ double upd(double A, double C, double c, double im, double ip, double jm,
+                                      double jp, double km, double kp) {
+  double s = __dadd_rn(im, ip);
+  s = __dadd_rn(s, jm);
+  s = __dadd_rn(s, jp);
+  s = __dadd_rn(s, km);
+  s = __dadd_rn(s, kp);
+  s = __dsub_rn(s, __dmul_rn(6.0, c));
+  return __dadd_rn(__dmul_rn(A, c), __dmul_rn(C, s));
+}
+
 __device__ __forceinline__ double2 lds2_u(uint32_t a) {
   double2 v;
   asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a) : "memory");
@@ -272,10 +286,16 @@ __device__ __forceinline__ bool t2b_ring_interior(const T2Item& I, int n, int x_
 // one work item of an E-row warp (MASK: item touches the lattice boundary;
 // PEER: the slab's edge output planes are also stored into the neighbour
 // slabs' halo planes, peer memory over NVLink -- the fused halo exchange)
-template <int S, int TB, bool STEP2, bool FASTC, bool MASK, bool PEER = false>
+// NRM (linear renormalisation pairs): the output is scaled by the pending
+// factor of the input (sc; by linearity S(f psi) = f S(psi) up to rounding)
+// and every step-2 warp writes the NORM partial of its output row and plane,
+// args.part[(plane * n + row - 1) * tiles_k + k-tile] (lane-pair sum, then
+// the xor butterfly), for k_plane_reduce + combine to form the next factor.
+template <int S, int TB, bool STEP2, bool FASTC, bool MASK, bool PEER = false, bool NRM = false>
 __device__ __forceinline__ void t2b_rows_item(const SweepArgs& args, const T2Item& I,
                                               uint32_t fb, uint32_t base, int w, int lane,
-                                              StageRot<S, T2BGeo<TB>::STAGE>& nx, uint32_t& g) {
+                                              StageRot<S, T2BGeo<TB>::STAGE>& nx, uint32_t& g,
+                                              double sc = 1.0) {
   using G = T2BGeo<TB>;
   using C = T2BCfg<S, TB>;
   constexpr uint32_t VOFF = G::PSI_STRIDE - BOXW * 8;  // V box starts one row lower
@@ -350,13 +370,24 @@ __device__ __forceinline__ void t2b_rows_item(const SweepArgs& args, const T2Ite
       const double2 rjp = lds2_u(rq + BOXW * 8);
       const double rkm = lds1_u(rq - 8);
       const double rkp = lds1_u(rq + 16);
-      const double o0 = upd(am.x, fm.x, qm.x, qmm.x, qw.x, rjm.x, rjp.x, rkm, qm.y);
-      const double o1 = upd(am.y, fm.y, qm.y, qmm.y, qw.y, rjm.y, rjp.y, qm.x, rkp);
+      double o0 = upd(am.x, fm.x, qm.x, qmm.x, qw.x, rjm.x, rjp.x, rkm, qm.y);
+      double o1 = upd(am.y, fm.y, qm.y, qmm.y, qw.y, rjm.y, rjp.y, qm.x, rkp);
+      if (NRM) {
+        o0 = __dmul_rn(o0, sc);
+        o1 = __dmul_rn(o1, sc);
+      }
       double* dst = args.out + doff;
       if (!MASK || ok1) {
         *reinterpret_cast<double2*>(dst) = make_double2(o0, o1);
       } else if (ok0) {
         *dst = o0;
+      }
+      if (NRM) {
+        double q = (!MASK || ok0) ? __dmul_rn(o0, o0) : 0.0;
+        if (!MASK || ok1) q = __fma_rn(o1, o1, q);
+        q = warp_sum(q);
+        if (lane == 0 && (!MASK || j <= n))
+          args.part[((long long)(p - 1) * n + (j - 1)) * args.tiles_k + ((I.k - 1) >> 6)] = q;
       }
       if (PEER) {
         const int z = p - 1;   // the output plane (uniform across the block)
@@ -393,8 +424,9 @@ __device__ __forceinline__ void t2b_rows_item(const SweepArgs& args, const T2Ite
   }
 }
 
-template <int S, int TB, bool STEP2, bool FASTC, bool PEER = false>
-__device__ __forceinline__ void t2b_rows(const SweepArgs& args, uint32_t sm0, int w, int lane) {
+template <int S, int TB, bool STEP2, bool FASTC, bool PEER = false, bool NRM = false>
+__device__ __forceinline__ void t2b_rows(const SweepArgs& args, uint32_t sm0, int w, int lane,
+                                         double sc = 1.0) {
   using C = T2BCfg<S, TB>;
   const uint32_t fb = sm0 + C::BAR_OFF;               // full[S], empty[S], rfull[4]
   const uint32_t base = sm0 + (uint32_t)(((w + 1) * BOXW + 2 * lane + 2) * 8);
@@ -419,9 +451,9 @@ __device__ __forceinline__ void t2b_rows(const SweepArgs& args, uint32_t sm0, in
   } else {
     t2b_for_items<TB>(args, [&](const T2Item& I) {
       if (t2b_row_interior(I, w, args.n, args.x_off))
-        t2b_rows_item<S, TB, STEP2, FASTC, false>(args, I, fb, base, w, lane, nx, g);
+        t2b_rows_item<S, TB, STEP2, FASTC, false, false, NRM>(args, I, fb, base, w, lane, nx, g, sc);
       else
-        t2b_rows_item<S, TB, STEP2, FASTC, true>(args, I, fb, base, w, lane, nx, g);
+        t2b_rows_item<S, TB, STEP2, FASTC, true, false, NRM>(args, I, fb, base, w, lane, nx, g, sc);
     });
   }
 }
@@ -513,7 +545,7 @@ __device__ __forceinline__ void t2b_ringw(const SweepArgs& args, uint32_t sm0, i
   });
 }
 
-template <int NST, int TB, bool FASTC, bool PEER = false>
+template <int NST, int TB, bool FASTC, bool PEER = false, bool NRM = false>
 __global__ void __launch_bounds__(T2BGeo<TB>::THREADS, T2BGeo<TB>::MINB)
     k_sweep2b(const __grid_constant__ CUtensorMap tm_psi, const __grid_constant__ CUtensorMap tm_v,
               const SweepArgs args) {
@@ -571,7 +603,9 @@ __global__ void __launch_bounds__(T2BGeo<TB>::THREADS, T2BGeo<TB>::MINB)
   } else if (warp == 0 || warp == TB + 1) {
     t2b_rows<S, TB, false, FASTC>(args, sm0, warp, lane);
   } else {
-    t2b_rows<S, TB, true, FASTC, PEER>(args, sm0, warp, lane);
+    static_assert(!(PEER && NRM), "no fused exchange in the renormalising pass");
+    const double sc = NRM ? *args.scale : 1.0;   // after pdl_wait: the predecessor's factor
+    t2b_rows<S, TB, true, FASTC, PEER, NRM>(args, sm0, warp, lane, sc);
   }
 }
 

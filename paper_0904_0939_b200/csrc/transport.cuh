@@ -472,11 +472,37 @@ int run_loop(std::vector<psg_slab*>& sl, Transport* tr, const psg_run_params* p,
     return (int)PSG_OK;
   };
   if (tr) tr->deep = false;
+  // linear renormalisation pairs (whole lattice): steps t, t+1 renormalised
+  // after t+1 run as one renormalising two-sweep pass (do_sweep2_nrm) when
+  // neither state inside the pair is measured nor re-imposed
+  const bool lin = whole && t2_ok && (p->flags & PSG_RUN_LINEAR_NORM) != 0;
+  auto meas_at = [&](int64_t t) {   // observables on the state entering sweep t
+    const int64_t state_idx = p->step_offset + t - 1;
+    return p->measure_every > 0 && state_idx > 0 && state_idx % p->measure_every == 0;
+  };
+  auto reimp_at = [&](int64_t t) {  // re-imposition after sweep t
+    const int64_t sidx = p->step_offset + t;
+    return p->reimpose_every > 0 && p->n_impose > 0 && sidx % p->reimpose_every == 0;
+  };
   for (int64_t t = 1; t <= p->steps; ++t) {
-    if (((whole && s0->use_march) || t2_ok) && s0->pending == s0->scal + S_ONE && plain(t)) {
+    if (lin && t + 1 <= p->steps && p->norm_every > 0 &&
+        (p->step_offset + t + 1) % p->norm_every == 0 && !meas_at(t) && !reimp_at(t) &&
+        !meas_at(t + 1)) {
+      rc = do_sweep2_nrm(s0);
+      if (rc) return rc;
+      ++t;
+      if (reimp_at(t)) {
+        for (int k = 0; k < p->n_impose && k < 3; ++k) {
+          rc = psg_impose(s0, p->impose_axis[k], p->impose_sign[k], 0);
+          if (rc) return rc;
+        }
+      }
+      continue;
+    }
+    if (t2_ok && s0->pending == s0->scal + S_ONE && plain(t)) {
       int64_t run = 1;
       while (t + run <= p->steps && plain(t + run)) ++run;
-      if ((!s0->use_march || tr) && run >= 2) {
+      if (run >= 2) {
         // pairs of plain steps: two sweeps per pass over HBM
         const int64_t pairs = run / 2;
         for (int64_t q = 0; q < pairs; ++q) {
@@ -484,18 +510,6 @@ int run_loop(std::vector<psg_slab*>& sl, Transport* tr, const psg_run_params* p,
           if (rc) return rc;
         }
         t += 2 * pairs - 1;
-        continue;
-      }
-      // the step after a run carries the measure / norm / impose: include it only if plain
-      if (whole && run >= 2) {
-        while (run > 0) {
-          const int chunk = (int)std::min<int64_t>(run, 1 << 20);
-          rc = do_march(s0, chunk);
-          if (rc) return rc;
-          run -= chunk;
-          t += chunk;
-        }
-        --t;
         continue;
       }
     }

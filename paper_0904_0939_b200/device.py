@@ -13,7 +13,8 @@ import ctypes
 import numpy as np
 
 from . import _lib
-from ._lib import F_CHECK, F_MEASURE, F_NORM, F_WRITE, NSCAL, RunParams, check, dptr, lptr
+from ._lib import (F_CHECK, F_MEASURE, F_NORM, F_WRITE, NSCAL, RUN_LINEAR_NORM, RunParams, check,
+                   dptr, lptr)
 from .errors import ConfigError, DeviceError, SingularCoefficientError
 from .lattice import LatticeSpec
 
@@ -187,10 +188,6 @@ class Slab:
         """Two-sweep passes alternate their chunk order (default 1)."""
         self.set_option(6, on)
 
-    def set_t2_pairs(self, on: int):
-        """Two tile rows per warp in the 16-row two-sweep pass (k_sweep2p)."""
-        self.set_option(7, on)
-
     def set_t2_seg(self, mode: int):
         """Work split of the two-sweep pass: 0 automatic, 1 round-robin chunk
         items, 2 one contiguous (tile, plane) range per block."""
@@ -211,10 +208,6 @@ class Slab:
     def set_zchunk(self, zc: int):
         """Planes per work item of the sweep (0 = automatic)."""
         self.tune(0, zc, 0)
-
-    def set_march(self, enable: bool):
-        """Persistent multi-step sweeps for runs of plain steps in run() (default off)."""
-        check(self._lib.psg_set_march(self._h, 1 if enable else 0))
 
     # ------------------------------------------------------------ data
     @property
@@ -280,10 +273,15 @@ class Slab:
         check(rc)
         self._v_owner = owner
 
-    def get_potential(self, first: int = 0, count: int | None = None) -> np.ndarray:
-        """Download potential planes (dense (count, ext, ext))."""
+    def get_potential(self, first: int = 0, count: int | None = None,
+                      out: np.ndarray | None = None) -> np.ndarray:
+        """Download potential planes (dense (count, ext, ext)), into ``out`` if given."""
         count = self.planes - first if count is None else count
-        out = np.empty((count, self.ext, self.ext))
+        if out is None:
+            out = np.empty((count, self.ext, self.ext))
+        elif (out.dtype != np.float64 or not out.flags.c_contiguous
+              or out.shape != (count, self.ext, self.ext)):
+            raise ConfigError("out must be C-contiguous float64 (count, ext, ext)")
         check(self._lib.psg_get_potential(self._h, dptr(out), first, count))
         return out
 
@@ -425,14 +423,14 @@ class Slab:
         check(self._lib.psg_resample(coarse._h, self._h, lptr(i0), dptr(frac)))
 
     def _run_params(self, steps, measure_every, norm_every, reimpose_every, constraints,
-                    step_offset, max_checks):
+                    step_offset, max_checks, linear_norm=False):
         constraints = list(constraints)
         if len(constraints) > 3:
             raise ConfigError("at most 3 parity constraints")
         axes = (ctypes.c_int32 * 3)(*([c[0] for c in constraints] + [0] * (3 - len(constraints))))
         signs = (ctypes.c_int32 * 3)(*([int(c[1]) for c in constraints] + [1] * (3 - len(constraints))))
         p = RunParams(steps, measure_every, norm_every, reimpose_every, step_offset,
-                      len(constraints), axes, signs, 0)
+                      len(constraints), axes, signs, RUN_LINEAR_NORM if linear_norm else 0)
         if max_checks is None:
             max_checks = steps // measure_every + 1 if measure_every > 0 else 0
         hist = np.zeros((max(max_checks, 1), 3 * self.n + 2))
@@ -445,14 +443,16 @@ class Slab:
 
     def run(self, steps: int, measure_every: int = 0, norm_every: int = 1,
             reimpose_every: int = 0, constraints=(), step_offset: int = 0,
-            max_checks: int | None = None):
+            max_checks: int | None = None, linear_norm: bool = False):
         """Fused fixed-step driver (psg_run).
 
         constraints: sequence of (storage axis, sign) applied in order every
-        reimpose_every sweeps.  Returns (state indices, plane sums [c, 3, N]
-        as num|den|r2, per-check status)."""
+        reimpose_every sweeps.  linear_norm: pairs of sweeps ending on a
+        renormalisation run as one renormalising two-sweep pass
+        (PSG_RUN_LINEAR_NORM; within roundoff of the per-step path).  Returns
+        (state indices, plane sums [c, 3, N] as num|den|r2, per-check status)."""
         p, max_checks, hist = self._run_params(steps, measure_every, norm_every, reimpose_every,
-                                               constraints, step_offset, max_checks)
+                                               constraints, step_offset, max_checks, linear_norm)
         nc = ctypes.c_int64()
         check(self._lib.psg_run(self._h, ctypes.byref(p), dptr(hist), max_checks, ctypes.byref(nc)))
         return self._unpack_hist(hist, nc.value)

@@ -295,7 +295,7 @@ def evolve_to_convergence(initial: Field3D, grid: PotentialGrid, tol: float = 1e
                           check_freq: int = 100, snap_freq: int | None = None, constraints=(),
                           max_steps: int = 1_000_000, max_snapshots: int = 8,
                           reimpose_freq: int | None = None,
-                          norm_every: int = 1) -> EvolutionState:
+                          norm_every: int = 1, exact: bool = False) -> EvolutionState:
     """Iterate sweeps until the convergence metric stops changing (evolve.py:206-272).
 
     Renormalises after every sweep, checks every ``check_freq`` sweeps on the
@@ -304,12 +304,20 @@ def evolve_to_convergence(initial: Field3D, grid: PotentialGrid, tol: float = 1e
     every ``reimpose_freq`` (default check_freq).  The sweeps between two
     host events run as one fused device loop (psg_run).
 
-    ``norm_every`` (extension; default 1 = the reference, bitwise) renormalises
+    ``norm_every`` (extension; default 1 = the reference's cadence) renormalises
     only every k-th sweep (k must divide check_freq and snap_freq, so checks
     and snapshots see a normalised state; k = check_freq is BASELINE's cadence).  The update is linear, so this changes the iterate only
     by roundoff (~1e-16 relative; SURVEY 8(c) measured 6.6e-16 after 2000
     steps at k = 100) while letting pairs of plain sweeps run as one two-sweep
     pass over HBM (faster at every size measured).
+
+    ``exact`` (extension): with the default per-sweep renormalisation, pairs
+    of sweeps run as one renormalising two-sweep pass (psg_run's linear
+    renormalisation pairs: the pending factor applied at the pass's store,
+    the norm of its output fused in; the normalisation after the pair's
+    first sweep is subsumed by linearity) -- within roundoff of the
+    reference, 2x fewer HBM passes.  ``exact=True`` runs every sweep with its
+    own renormalisation, bitwise the reference's arithmetic.
     """
     from .device import Slab
 
@@ -332,7 +340,7 @@ def evolve_to_convergence(initial: Field3D, grid: PotentialGrid, tol: float = 1e
         step_count, converged, checks, snapshots = converge_on_slab(
             slab, grid, tol=tol, check_freq=check_freq, snap_freq=snap_freq,
             constraints=constraints, max_steps=max_steps, max_snapshots=max_snapshots,
-            reimpose_freq=reimpose_freq, norm_every=norm_every)
+            reimpose_freq=reimpose_freq, norm_every=norm_every, linear_norm=not exact)
         return EvolutionState(psi=Field3D(spec, slab.get_field()), tau=step_count * spec.dtau,
                               step_count=step_count, snapshots=snapshots, checks=checks,
                               converged=converged, constraints=constraints,
@@ -343,7 +351,7 @@ def evolve_to_convergence(initial: Field3D, grid: PotentialGrid, tol: float = 1e
 
 def converge_on_slab(slab, grid: PotentialGrid, *, tol: float, check_freq: int, snap_freq: int,
                      constraints=(), max_steps: int, max_snapshots: int, reimpose_freq: int,
-                     norm_every: int = 1):
+                     norm_every: int = 1, linear_norm: bool = True):
     """The evolve_to_convergence loop on a device-resident whole-lattice slab
     (its field and potential already in place); leaves the final state on the
     slab.  Returns (step_count, converged, checks, snapshots)."""
@@ -373,7 +381,7 @@ def converge_on_slab(slab, grid: PotentialGrid, *, tol: float, check_freq: int, 
             nxt = min(nxt, (s // snap_freq + 1) * snap_freq)
         slab.run(nxt - s, measure_every=0, norm_every=norm_every,
                  reimpose_every=reimpose_freq if pairs else 0, constraints=pairs,
-                 step_offset=s)
+                 step_offset=s, linear_norm=linear_norm)
         _raise_status(slab.status(), f"before step {nxt}")
         s = nxt
         if s % snap_freq == 0 and len(snapshots) < max_snapshots:
@@ -383,13 +391,22 @@ def converge_on_slab(slab, grid: PotentialGrid, *, tol: float, check_freq: int, 
 
 def evolve_fixed(initial: Field3D, grid: PotentialGrid, steps: int, measure_every: int,
                  norm_every: int = 1, constraints=(), reimpose_every: int | None = None,
-                 slab=None) -> EvolutionState:
+                 slab=None, out: np.ndarray | None = None,
+                 timings: dict | None = None) -> EvolutionState:
     """Fixed-step run with the observables fused into the sweeps (BASELINE
     configurations: no convergence decisions, so no host round trip until the
     end).  Checks follow evolve_to_convergence's schedule (state indices
     m, 2m, ... < steps); their scalars come from the device plane sums with
     np.sum.  ``norm_every`` > 1 renormalises less often (BASELINE: at
-    measurement steps); the factor is still folded into the next sweep."""
+    measurement steps); the factor is still folded into the next sweep.
+
+    ``out`` (extension): a C-contiguous float64 padded array the final state
+    is downloaded into (it may be ``initial.values`` itself: the start is on
+    the device before the run) -- a 2048^3 run then needs two host fields
+    (psi, V), not three.  ``timings`` (extension): filled with the
+    perf_counter seconds of the phases (upload, run, download)."""
+    import time
+
     from .device import Slab
 
     spec = initial.spec
@@ -397,23 +414,30 @@ def evolve_fixed(initial: Field3D, grid: PotentialGrid, steps: int, measure_ever
     pairs = _constraint_pairs(constraints)
     if reimpose_every is None:
         reimpose_every = measure_every
+    t0 = time.perf_counter()
     own = slab is None
     if own:
         slab = Slab(spec)
         slab.set_field(_dirichlet_start(initial))
     slab.load_grid(grid)
     try:
+        slab.sync()
+        t1 = time.perf_counter()
         idx, sums, status = slab.run(steps, measure_every=measure_every, norm_every=norm_every,
                                      reimpose_every=reimpose_every if pairs else 0,
                                      constraints=pairs)
         _raise_status(slab.status(), "during the run")
+        t2 = time.perf_counter()
         checks = []
         for st, sm in zip(idx, sums):
             rec = _record_from_sums(sm[0], sm[1], sm[2], grid, spec)
             rec.step = int(st)
             rec.tau = int(st) * spec.dtau
             checks.append(rec)
-        return EvolutionState(psi=Field3D(spec, slab.get_field()), tau=steps * spec.dtau,
+        final = slab.get_field(out=out)
+        if timings is not None:
+            timings.update(upload_s=t1 - t0, run_s=t2 - t1, download_s=time.perf_counter() - t2)
+        return EvolutionState(psi=Field3D(spec, final), tau=steps * spec.dtau,
                               step_count=steps, checks=checks, converged=False,
                               constraints=constraints, sweeps_started=steps)
     finally:

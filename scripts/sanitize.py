@@ -39,6 +39,24 @@ def main():
         s.run(4, 0, 0)
         out = s.get_field()
         assert np.isfinite(out).all()
+    # single-buffer slab: chunked passes, in-place parity pairs on every axis
+    with Slab(spec, single_buffer=True, chunk=5) as s:
+        s.set_field(psi)
+        s.set_potential(v)
+        s.run(9, measure_every=4, norm_every=4)
+        for ax in (0, 1, 2):
+            s.impose(ax, -1, 0)
+        s.impose(2, 1, 1)
+        assert np.isfinite(s.get_field()).all()
+    # resample coarse -> fine (k_resample)
+    from paper_0904_0939_b200.multires import resample_indices
+
+    fspec = LatticeSpec(N=2 * n, a=spec.a / 2, m=1.0, dtau=(spec.a / 2) ** 2 / 4.0)
+    i0, frac = resample_indices(spec, fspec)
+    with Slab(spec) as sc, Slab(fspec) as sf:
+        sc.set_field(psi)
+        sf.resample_from(sc, i0, frac)
+        assert np.isfinite(sf.get_field()).all()
     widths = (n // 3, n // 3, n - 2 * (n // 3))
     slabs, lo = [], 1
     for w in widths:

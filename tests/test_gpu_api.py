@@ -485,7 +485,7 @@ class TestSlabEngine:
         grid = harmonic(spec)
         init = fill_random_gaussian(allocate(spec), 7)
         serial = evolve_to_convergence(init, grid, tol=1e-300, check_freq=25, max_steps=120,
-                                       max_snapshots=0)
+                                       max_snapshots=0, exact=True)
         par = evolve_parallel(grid, workers=workers, initial=init, tol=1e-300, check_freq=25,
                               max_steps=120, max_snapshots=0)
         assert np.array_equal(par.psi.values, serial.psi.values)
@@ -520,7 +520,7 @@ class TestSlabEngine:
         for c in cs:
             impose_inplace(init.values, spec.N, c)
         serial = evolve_to_convergence(init, grid, tol=1e-300, check_freq=20, max_steps=80,
-                                       constraints=cs, max_snapshots=0)
+                                       constraints=cs, max_snapshots=0, exact=True)
         par = evolve_parallel(grid, workers=3, initial=init, tol=1e-300, check_freq=20,
                               max_steps=80, constraints=cs, max_snapshots=0)
         assert np.array_equal(par.psi.values, serial.psi.values)
@@ -618,12 +618,44 @@ def test_convergence_with_sparse_normalisation(gpu_lib):
     grid = harmonic(spec)
     init = fill_random_gaussian(allocate(spec), 21)
     ref = evolve_to_convergence(init, grid, tol=1e-6, check_freq=50, max_steps=2000,
-                                max_snapshots=0)
-    fast = evolve_to_convergence(init, grid, tol=1e-6, check_freq=50, max_steps=2000,
-                                 max_snapshots=0, norm_every=50)
-    assert fast.step_count == ref.step_count and fast.converged == ref.converged
-    for a, b in zip(fast.checks, ref.checks):
-        assert abs(a.energy - b.energy) <= 1e-12 * abs(b.energy)
-        assert abs(a.r_rms - b.r_rms) <= 1e-12 * abs(b.r_rms)
-    d = np.max(np.abs(fast.psi.values - ref.psi.values))
-    assert d <= 1e-12 * np.max(np.abs(ref.psi.values))
+                                max_snapshots=0, exact=True)
+    for kw in (dict(norm_every=50), dict()):   # sparse norms; linear renormalisation pairs
+        fast = evolve_to_convergence(init, grid, tol=1e-6, check_freq=50, max_steps=2000,
+                                     max_snapshots=0, **kw)
+        assert fast.step_count == ref.step_count and fast.converged == ref.converged
+        for a, b in zip(fast.checks, ref.checks):
+            assert abs(a.energy - b.energy) <= 1e-12 * abs(b.energy)
+            assert abs(a.r_rms - b.r_rms) <= 1e-12 * abs(b.r_rms)
+        d = np.max(np.abs(fast.psi.values - ref.psi.values))
+        assert d <= 1e-12 * np.max(np.abs(ref.psi.values))
+
+
+@pytest.mark.parametrize("n", [8, 33, 64, 130])
+def test_linear_norm_pairs_match_per_step(gpu_lib, n):
+    """psg_run's linear renormalisation pairs (the default of
+    evolve_to_convergence): one two-sweep pass per pair with the pending factor
+    applied at the store and the output's norm fused in, against the exact
+    per-step path (k_sweep with fused NORM every sweep, the reference's
+    arithmetic bitwise) -- odd step counts, checks, re-imposition, an odd
+    offset; fields to 1e-13 of their maximum, norms to 1e-14."""
+    from paper_0904_0939_b200.device import Slab
+
+    spec = LatticeSpec(N=n, a=0.4, m=1.0, dtau=0.4 * 0.4 / 4.0)
+    grid = harmonic(spec)
+    init = fill_random_gaussian(allocate(spec), 5)
+    runs = []
+    for lin in (False, True):
+        with Slab(spec) as s:
+            s.set_field(init.values)
+            s.load_grid(grid)
+            l0 = s.launches()
+            idx, sums, st = s.run(37, measure_every=10, norm_every=1, reimpose_every=12,
+                                  constraints=[(2, -1)], step_offset=3, linear_norm=lin)
+            launches = s.launches() - l0
+            assert not st.any() and s.status() == 0
+            runs.append((s.get_field(), idx, sums, launches))
+    (f0, i0, s0, l0), (f1, i1, s1, l1) = runs
+    assert list(i0) == list(i1)
+    assert np.abs(f1 - f0).max() <= 1e-13 * np.abs(f0).max()
+    np.testing.assert_allclose(s1, s0, rtol=1e-12, atol=1e-300)
+    assert l1 < l0     # pairs went through the renormalising pass

@@ -127,7 +127,7 @@ def test_evolve_parallel_snapshot_on_converging_step(gpu_lib, workers):
     init = np.zeros((spec.N + 2,) * 3)
     init[1:-1, 1:-1, 1:-1] = rng.uniform(-0.5, 0.5, (spec.N,) * 3)
     kw = dict(tol=1e-5, check_freq=10, snap_freq=10, max_snapshots=1000, max_steps=20000)
-    ser = evolve_to_convergence(Field3D(spec, init.copy()), grid, **kw)
+    ser = evolve_to_convergence(Field3D(spec, init.copy()), grid, exact=True, **kw)
     par = evolve_parallel(grid, workers=workers, initial=Field3D(spec, init.copy()), **kw)
     assert ser.converged and par.converged
     assert par.step_count == ser.step_count

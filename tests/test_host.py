@@ -264,15 +264,14 @@ def test_slab_field_bytes_c5_sizes():
 
 
 def test_bench_helpers():
-    """bench.py's weak-scaling sizes and its model of psg_run's pass schedule."""
-    import bench
+    """bench.py's model of psg_run's pass schedule, the config dict both arms
+    print, and the --gpus guard."""
+    import subprocess
+    import sys
 
-    assert bench.weak_n(256, 1) == 256
-    for m in (2, 4, 8):
-        n = bench.weak_n(256, m)
-        assert n % m == 0 and n % 64 == 0
-        assert abs(n ** 3 / m - 256 ** 3) / 256 ** 3 < 0.2
-    assert [bench.weak_n(256, m) for m in (2, 4, 8)] == [320, 384, 512]
+    import bench
+    from paper_0904_0939_b200 import workloads
+
     # pairing rule: runs of plain steps in pairs; measure (state index % m == 0)
     # and norm (step % m == 0) steps single
     passes, singles = bench.t2_schedule(4000, 100, 500)
@@ -282,6 +281,19 @@ def test_bench_helpers():
     assert singles == 18
     passes, singles = bench.t2_schedule(10, 0, 0)
     assert (passes, singles) == (5, 0)
+    # the default workload is the north star's 2048^3 lattice, strong scaling
+    assert bench.DEFAULT_CONFIG == "C5"
+    w = workloads.CONFIGS["C5"]
+    cfg = bench.bench_config(w, 1)
+    assert cfg["N"] == 2048 and cfg["scaling"] == "strong" and cfg["parallelism"] == "single GPU"
+    assert bench.bench_config(w, 8)["parallelism"] == "z-slabs x8 of 256 planes"
+    # both arms print the same config for the same command (no timing inside)
+    assert bench.bench_config(w, 4) == bench.bench_config(w, 4)
+    assert bench.bench_config(workloads.CONFIGS["C2"], 1)["scaling"] == "weak"
+    # more ranks than visible GPUs is an error (this host has none)
+    r = subprocess.run([sys.executable, "bench.py", "--gpus", "9", "--no-cpu"], cwd=ROOT,
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 2 and "GPU(s) visible" in r.stderr
 
 
 def test_qwf1_bytes_match_reference_files(tmp_path):
