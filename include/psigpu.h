@@ -416,7 +416,9 @@ int psg_tune(psg_slab* s, int blocks_per_sm, int zchunk, int stages);
  * two-sweep pass also stores its edge output planes into the neighbouring
  * slabs' halo planes through peer memory (NVLink between GPUs) instead of a
  * separate copy; needs W >= 4 and peer access, else the copies are used
- * (bitwise unchanged). */
+ * (bitwise unchanged), 12 = persistent brick kernel (k_small) for runs of plain
+ * sweeps of a whole lattice with N <= 64, N % 16 == 0 (default 1; bitwise
+ * unchanged). */
 int psg_set_option(psg_slab* s, int option, int value);
 
 /* Enable / disable two sweeps per HBM pass (temporal blocking) for pairs of

@@ -225,3 +225,40 @@ __global__ void __launch_bounds__(256)
   pdl_wait();
   combine_body(plane_sums, n, qmask, a3, scal, hist_rec, bad, sm);
 }
+
+// Total of a renormalising pass's NORM slots (one per step-2 warp and launch)
+// in a fixed order -- per thread a strided sequential sum, then a fixed
+// shared-memory tree -- and the factor / status the combine would form
+// (scal[S_N2], scal[S_FACTOR], scal[S_STATUS]).  One block.
+constexpr int NT_THREADS = 512;
+__global__ void __launch_bounds__(NT_THREADS)
+    k_norm_total(const double* __restrict__ slots, long long count, double a3, double* scal,
+                 const int* bad) {
+  __shared__ double red[NT_THREADS];
+  pdl_launch_dependents();
+  pdl_wait();
+  double acc = 0.0;
+  for (long long i = threadIdx.x; i < count; i += NT_THREADS) acc = __dadd_rn(acc, slots[i]);
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int w = NT_THREADS / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] = __dadd_rn(red[threadIdx.x], red[threadIdx.x + w]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    double status = scal[S_STATUS];
+    const double n2 = __dmul_rn(red[0], a3);
+    scal[S_N2] = n2;
+    if (n2 == 0.0) {
+      if (status == 0.0) status = 3.0;
+      scal[S_FACTOR] = 1.0;
+    } else if (!finite_d(n2)) {
+      if (status == 0.0) status = 4.0;
+      scal[S_FACTOR] = 1.0;
+    } else {
+      scal[S_FACTOR] = __ddiv_rn(1.0, __dsqrt_rn(n2));
+    }
+    if (bad && __ldcg(bad) && status == 0.0) status = 4.0;
+    scal[S_STATUS] = status;
+  }
+}

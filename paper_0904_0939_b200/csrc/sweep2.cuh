@@ -287,15 +287,17 @@ __device__ __forceinline__ bool t2b_ring_interior(const T2Item& I, int n, int x_
 // PEER: the slab's edge output planes are also stored into the neighbour
 // slabs' halo planes, peer memory over NVLink -- the fused halo exchange)
 // NRM (linear renormalisation pairs): the output is scaled by the pending
-// factor of the input (sc; by linearity S(f psi) = f S(psi) up to rounding)
-// and every step-2 warp writes the NORM partial of its output row and plane,
-// args.part[(plane * n + row - 1) * tiles_k + k-tile] (lane-pair sum, then
-// the xor butterfly), for k_plane_reduce + combine to form the next factor.
+// factor of the input (fnorm; by linearity S(f psi) = f S(psi) up to rounding)
+// and every step-2 lane accumulates the squares of its outputs over the whole
+// launch (qacc, in a fixed order); one xor butterfly per warp at the end
+// writes args.part[nslot + block * TB + warp - 1] for k_norm_total.  No
+// per-plane sums: a whole-lattice slab needs only the total (per-plane
+// butterflies cost +31 % instructions, measured).
 template <int S, int TB, bool STEP2, bool FASTC, bool MASK, bool PEER = false, bool NRM = false>
 __device__ __forceinline__ void t2b_rows_item(const SweepArgs& args, const T2Item& I,
                                               uint32_t fb, uint32_t base, int w, int lane,
                                               StageRot<S, T2BGeo<TB>::STAGE>& nx, uint32_t& g,
-                                              double sc = 1.0) {
+                                              double fnorm = 1.0, double* qacc = nullptr) {
   using G = T2BGeo<TB>;
   using C = T2BCfg<S, TB>;
   constexpr uint32_t VOFF = G::PSI_STRIDE - BOXW * 8;  // V box starts one row lower
@@ -373,8 +375,8 @@ __device__ __forceinline__ void t2b_rows_item(const SweepArgs& args, const T2Ite
       double o0 = upd(am.x, fm.x, qm.x, qmm.x, qw.x, rjm.x, rjp.x, rkm, qm.y);
       double o1 = upd(am.y, fm.y, qm.y, qmm.y, qw.y, rjm.y, rjp.y, qm.x, rkp);
       if (NRM) {
-        o0 = __dmul_rn(o0, sc);
-        o1 = __dmul_rn(o1, sc);
+        o0 = __dmul_rn(o0, fnorm);
+        o1 = __dmul_rn(o1, fnorm);
       }
       double* dst = args.out + doff;
       if (!MASK || ok1) {
@@ -382,12 +384,9 @@ __device__ __forceinline__ void t2b_rows_item(const SweepArgs& args, const T2Ite
       } else if (ok0) {
         *dst = o0;
       }
-      if (NRM) {
-        double q = (!MASK || ok0) ? __dmul_rn(o0, o0) : 0.0;
-        if (!MASK || ok1) q = __fma_rn(o1, o1, q);
-        q = warp_sum(q);
-        if (lane == 0 && (!MASK || j <= n))
-          args.part[((long long)(p - 1) * n + (j - 1)) * args.tiles_k + ((I.k - 1) >> 6)] = q;
+      if (NRM) {   // this lane's share of the output's norm, summed over the launch
+        if (!MASK || ok0) *qacc = __fma_rn(o0, o0, *qacc);
+        if (!MASK || ok1) *qacc = __fma_rn(o1, o1, *qacc);
       }
       if (PEER) {
         const int z = p - 1;   // the output plane (uniform across the block)
@@ -426,7 +425,7 @@ __device__ __forceinline__ void t2b_rows_item(const SweepArgs& args, const T2Ite
 
 template <int S, int TB, bool STEP2, bool FASTC, bool PEER = false, bool NRM = false>
 __device__ __forceinline__ void t2b_rows(const SweepArgs& args, uint32_t sm0, int w, int lane,
-                                         double sc = 1.0) {
+                                         double fnorm = 1.0) {
   using C = T2BCfg<S, TB>;
   const uint32_t fb = sm0 + C::BAR_OFF;               // full[S], empty[S], rfull[4]
   const uint32_t base = sm0 + (uint32_t)(((w + 1) * BOXW + 2 * lane + 2) * 8);
@@ -449,12 +448,19 @@ __device__ __forceinline__ void t2b_rows(const SweepArgs& args, uint32_t sm0, in
     // IPC transport's post kernel, which fences at system scope and then
     // publishes its counter)
   } else {
+    double qacc = 0.0;
     t2b_for_items<TB>(args, [&](const T2Item& I) {
       if (t2b_row_interior(I, w, args.n, args.x_off))
-        t2b_rows_item<S, TB, STEP2, FASTC, false, false, NRM>(args, I, fb, base, w, lane, nx, g, sc);
+        t2b_rows_item<S, TB, STEP2, FASTC, false, false, NRM>(args, I, fb, base, w, lane, nx, g, fnorm,
+                                                             &qacc);
       else
-        t2b_rows_item<S, TB, STEP2, FASTC, true, false, NRM>(args, I, fb, base, w, lane, nx, g, sc);
+        t2b_rows_item<S, TB, STEP2, FASTC, true, false, NRM>(args, I, fb, base, w, lane, nx, g, fnorm,
+                                                            &qacc);
     });
+    if constexpr (NRM && STEP2) {
+      qacc = warp_sum(qacc);
+      if (lane == 0) args.part[args.nslot + blockIdx.x * TB + (w - 1)] = qacc;
+    }
   }
 }
 
@@ -604,8 +610,8 @@ __global__ void __launch_bounds__(T2BGeo<TB>::THREADS, T2BGeo<TB>::MINB)
     t2b_rows<S, TB, false, FASTC>(args, sm0, warp, lane);
   } else {
     static_assert(!(PEER && NRM), "no fused exchange in the renormalising pass");
-    const double sc = NRM ? *args.scale : 1.0;   // after pdl_wait: the predecessor's factor
-    t2b_rows<S, TB, true, FASTC, PEER, NRM>(args, sm0, warp, lane, sc);
+    const double fnorm = NRM ? *args.scale : 1.0;   // after pdl_wait: the predecessor's factor
+    t2b_rows<S, TB, true, FASTC, PEER, NRM>(args, sm0, warp, lane, fnorm);
   }
 }
 

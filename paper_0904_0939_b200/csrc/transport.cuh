@@ -502,6 +502,13 @@ int run_loop(std::vector<psg_slab*>& sl, Transport* tr, const psg_run_params* p,
     if (t2_ok && s0->pending == s0->scal + S_ONE && plain(t)) {
       int64_t run = 1;
       while (t + run <= p->steps && plain(t + run)) ++run;
+      if (whole && run >= SMALL_MIN_RUN && small_ok(s0)) {
+        // a small lattice: the whole run of plain sweeps in one persistent launch
+        rc = do_small(s0, run);
+        if (rc) return rc;
+        t += run - 1;
+        continue;
+      }
       if (run >= 2) {
         // pairs of plain steps: two sweeps per pass over HBM
         const int64_t pairs = run / 2;

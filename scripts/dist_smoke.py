@@ -41,7 +41,7 @@ def main():
                              native=native)
         if rank == 0:
             ref = evolve_to_convergence(init, grid, tol=1e-300, check_freq=20, max_steps=100,
-                                        max_snapshots=0, constraints=cs)
+                                        max_snapshots=0, constraints=cs, exact=True)
             same = np.array_equal(st.psi.values, ref.psi.values)
             e_same = [c.energy for c in st.checks] == [c.energy for c in ref.checks]
             print(f"dist_smoke world={world} native={native}: psi bitwise {same}, energies "
@@ -55,7 +55,7 @@ def main():
                          check_freq=10, max_steps=4000, max_snapshots=0, constraints=cs)
     if rank == 0:
         ref = evolve_to_convergence(init, grid, tol=1e-5, check_freq=10, max_steps=4000,
-                                    max_snapshots=0, constraints=cs)
+                                    max_snapshots=0, constraints=cs, exact=True)
         same = (np.array_equal(st.psi.values, ref.psi.values) and st.step_count == ref.step_count
                 and st.converged == ref.converged)
         print(f"dist_smoke converging: bitwise {same}, steps {st.step_count} vs "

@@ -41,6 +41,41 @@ def test_sweep_bitwise(gpu_lib, n):
     assert np.array_equal(got, want)
 
 
+@pytest.mark.parametrize("n", [16, 32, 48, 64])
+def test_small_lattice_persistent_sweeps_bitwise(gpu_lib, n):
+    """k_small (one persistent launch for a run of plain sweeps of a small
+    lattice, bricks exchanging faces through global memory) is bitwise the
+    per-launch path, with norm / measure steps cutting the runs, and the
+    oracle's plain sweeps."""
+    spec, psi, v = _case(n, 700 + n, pad=0.0)
+    outs = []
+    for small in (0, 1):
+        with Slab(spec) as s:
+            s.set_option(12, small)
+            s.set_field(psi)
+            s.set_potential(v)
+            l0 = s.launches()
+            idx, sums, st = s.run(57, measure_every=20, norm_every=20, step_offset=1)
+            assert not st.any()
+            outs.append((s.get_field(), idx, sums, s.launches() - l0))
+    assert np.array_equal(outs[0][0], outs[1][0])
+    assert list(outs[0][1]) == list(outs[1][1])
+    assert np.array_equal(outs[0][2], outs[1][2])
+    assert outs[1][3] < outs[0][3]
+    want = psi.copy()
+    for _ in range(9):
+        out = want.copy()
+        O.stencil_update_v(want, v, spec.dtau, spec.m, spec.a, out, 1, n)
+        want = out
+    with Slab(spec) as s:
+        s.set_field(psi)
+        s.set_potential(v)
+        l0 = s.launches()
+        s.run(9, 0, 0)
+        assert s.launches() - l0 == 1
+        assert np.array_equal(s.get_field(), want)
+
+
 def test_new_potential_clears_coefficient_mode(gpu_lib):
     """Precomputed A/C arrays (psg_set_coefficients) are used until the next V
     upload or fill: a slab given A/C for V1 and then V2 sweeps with V2's
@@ -147,38 +182,11 @@ def test_coefficient_division_is_ieee(gpu_lib, lo, hi):
         assert bad.value == 0
 
 
-@pytest.mark.parametrize("n,steps,every", [(16, 50, 0), (40, 123, 20), (64, 300, 100),
-                                           (130, 64, 30)])
-def test_march_matches_single_step_sweeps(gpu_lib, n, steps, every):
-    """The persistent multi-step sweep (dataflow flags across steps) gives the
-    same bits as one launch per sweep, including around norm/measure steps."""
-    spec = LatticeSpec(N=n, a=0.3, m=1.0, dtau=0.3 * 0.3 / 4.0)
-    rng = np.random.default_rng(n)
-    ext = n + 2
-    psi0 = np.zeros((ext,) * 3)
-    psi0[1:-1, 1:-1, 1:-1] = rng.uniform(-0.5, 0.5, (n, n, n))
-    v = np.zeros((ext,) * 3)
-    v[1:-1, 1:-1, 1:-1] = rng.uniform(-1.0, 3.0, (n, n, n))
-    out = []
-    for march in (False, True):
-        with Slab(spec) as s:
-            s.set_march(march)
-            s.set_field(psi0)
-            s.set_potential(v)
-            idx, sums, status = s.run(steps, measure_every=every, norm_every=every)
-            if march:
-                assert s.launches() < steps  # plain steps were batched
-            out.append((s.get_field(), sums))
-    assert np.array_equal(out[0][0], out[1][0])
-    assert np.array_equal(out[0][1], out[1][1])
-
-
 @pytest.mark.parametrize("n,steps,every", [(8, 9, 0), (16, 50, 0), (40, 123, 20), (64, 300, 100),
                                            (100, 61, 0), (130, 64, 30), (256, 20, 10)])
-@pytest.mark.parametrize("rows,stages,pairs,seg", [(8, 6, 0, 1), (16, 6, 0, 1), (16, 9, 0, 1),
-                                                   (16, 6, 1, 1), (16, 6, 0, 2), (16, 6, 1, 2),
-                                                   (16, 6, 0, 0)])
-def test_two_step_pass_matches_single_steps(gpu_lib, n, steps, every, rows, stages, pairs, seg):
+@pytest.mark.parametrize("rows,stages,seg", [(8, 6, 1), (16, 6, 1), (16, 9, 1), (16, 6, 2),
+                                             (16, 6, 0)])
+def test_two_step_pass_matches_single_steps(gpu_lib, n, steps, every, rows, stages, seg):
     """Temporal blocking (two sweeps per HBM pass, intermediate plane ring in
     shared memory) gives the same bits as one launch per sweep."""
     spec = LatticeSpec(N=n, a=0.3, m=1.0, dtau=0.3 * 0.3 / 4.0)
@@ -191,11 +199,10 @@ def test_two_step_pass_matches_single_steps(gpu_lib, n, steps, every, rows, stag
     out = []
     for t2 in (False, True):
         with Slab(spec) as s:
-            s.set_march(False)
+            s.set_option(12, 0)   # the two-sweep pass, not the small-lattice kernel
             s.set_temporal(t2)
             s.set_t2_rows(rows)
             s.set_t2_stages(stages)
-            s.set_t2_pairs(pairs)
             s.set_t2_seg(seg)
             s.set_field(psi0)
             s.set_potential(v)
@@ -209,8 +216,8 @@ def test_two_step_pass_matches_single_steps(gpu_lib, n, steps, every, rows, stag
 
 @pytest.mark.parametrize("n,rows,wide,force", [(40, 16, False, True), (72, 16, True, False),
                                                (72, 8, True, False), (130, 16, True, True)])
-@pytest.mark.parametrize("stages,pairs", [(6, 0), (9, 0), (6, 1)])
-def test_two_step_pass_coefficient_paths(gpu_lib, n, rows, wide, force, stages, pairs):
+@pytest.mark.parametrize("stages", [6, 9])
+def test_two_step_pass_coefficient_paths(gpu_lib, n, rows, wide, force, stages):
     """The two-step pass's coefficient paths: without the per-plane range vote
     (every d = 1 + hV in [0.25, 4), checked at upload), with it (option 4),
     and potentials reaching d >= 4 or d < 0.25 (IEEE division per site) all
@@ -230,12 +237,10 @@ def test_two_step_pass_coefficient_paths(gpu_lib, n, rows, wide, force, stages, 
     out = []
     for t2 in (False, True):
         with Slab(spec) as s:
-            s.set_march(False)
             s.set_temporal(t2)
             s.set_t2_rows(rows)
             s.set_option(4, 1 if force else 0)
             s.set_t2_stages(stages)
-            s.set_t2_pairs(pairs)
             s.set_field(psi0)
             s.set_potential(v)
             idx, sums, status = s.run(40, measure_every=20, norm_every=20)

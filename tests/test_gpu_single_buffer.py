@@ -146,8 +146,6 @@ def test_single_buffer_memory_and_limits(gpu_lib):
         assert 0 < avail <= total and total > 100e9   # a B200's HBM
         with pytest.raises(ConfigError):
             one.sweep(1, n // 2, F_WRITE)       # chunk order needs the whole sweep
-        with pytest.raises(ConfigError):
-            one.set_march(True)
     with pytest.raises(ConfigError):
         Slab(spec, w=32, x_lo=1, single_buffer=True)
 
