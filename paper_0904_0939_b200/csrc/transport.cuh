@@ -288,7 +288,11 @@ inline void split_ranges(const psg_slab* s, bool l, bool r, int depth, int64_t& 
 // the interior planes; nothing to post if the deep halos of the current
 // buffers are already in flight), then the edge planes
 int multi_sweep(std::vector<psg_slab*>& sl, Transport* tr, unsigned flags, bool write) {
-  int rc = tr->deep ? PSG_OK : tr->post(1);
+  int rc = PSG_OK;
+  if (!tr->deep) {
+    NvtxRange nv("psg:halo_post");
+    rc = tr->post(1);
+  }
   if (rc) return rc;
   for (size_t r = 0; r < sl.size(); ++r) {
     CU_TRY(cudaSetDevice(sl[r]->device));
@@ -327,7 +331,11 @@ int multi_sweep(std::vector<psg_slab*>& sl, Transport* tr, unsigned flags, bool 
 // (cuStreamWaitValue64), so it runs while the launch is still updating the
 // interior.  One exchange per two sweeps; no host in the loop.
 int multi_sweep2(std::vector<psg_slab*>& sl, Transport* tr) {
-  int rc = tr->deep ? PSG_OK : tr->post(2);
+  int rc = PSG_OK;
+  if (!tr->deep) {
+    NvtxRange nv("psg:halo_post");
+    rc = tr->post(2);
+  }
   if (rc) return rc;
   rc = tr->wait();
   if (rc) return rc;
@@ -488,7 +496,7 @@ int run_loop(std::vector<psg_slab*>& sl, Transport* tr, const psg_run_params* p,
     if (lin && t + 1 <= p->steps && p->norm_every > 0 &&
         (p->step_offset + t + 1) % p->norm_every == 0 && !meas_at(t) && !reimp_at(t) &&
         !meas_at(t + 1)) {
-      rc = do_sweep2_nrm(s0);
+      { NvtxRange nv("psg:pass2_renorm"); rc = do_sweep2_nrm(s0); }
       if (rc) return rc;
       ++t;
       if (reimp_at(t)) {
@@ -504,7 +512,7 @@ int run_loop(std::vector<psg_slab*>& sl, Transport* tr, const psg_run_params* p,
       while (t + run <= p->steps && plain(t + run)) ++run;
       if (whole && run >= SMALL_MIN_RUN && small_ok(s0)) {
         // a small lattice: the whole run of plain sweeps in one persistent launch
-        rc = do_small(s0, run);
+        { NvtxRange nv("psg:small_run"); rc = do_small(s0, run); }
         if (rc) return rc;
         t += run - 1;
         continue;
@@ -513,6 +521,7 @@ int run_loop(std::vector<psg_slab*>& sl, Transport* tr, const psg_run_params* p,
         // pairs of plain steps: two sweeps per pass over HBM
         const int64_t pairs = run / 2;
         for (int64_t q = 0; q < pairs; ++q) {
+          NvtxRange nv("psg:pass2");
           rc = tr ? multi_sweep2(sl, tr) : do_sweep2(s0);
           if (rc) return rc;
         }
@@ -528,7 +537,10 @@ int run_loop(std::vector<psg_slab*>& sl, Transport* tr, const psg_run_params* p,
     const bool norm = p->norm_every > 0 && sidx % p->norm_every == 0;
     if (meas) flags |= PSG_F_MEASURE;
     if (norm) flags |= PSG_F_NORM;
-    rc = tr ? multi_sweep(sl, tr, flags, true) : do_sweep(s0, 1, s0->w, flags, true);
+    {
+      NvtxRange nv(flags & PSG_F_MEASURE ? "psg:sweep_measure" : "psg:sweep");
+      rc = tr ? multi_sweep(sl, tr, flags, true) : do_sweep(s0, 1, s0->w, flags, true);
+    }
     if (rc) return rc;
     const unsigned q = qmask_of(flags);
     if (q) {
@@ -540,7 +552,10 @@ int run_loop(std::vector<psg_slab*>& sl, Transport* tr, const psg_run_params* p,
           return do_reduce(s, 1, s->w, q, false, nullptr);
         });
         if (rc) return rc;
-        rc = tr->allreduce();
+        {
+          NvtxRange nv("psg:allreduce");
+          rc = tr->allreduce();
+        }
         if (rc) return rc;
         rc = set_all([&](psg_slab* s) { return do_combine(s, q, meas ? s->hist_dev + nc * rec : nullptr); });
       } else {

@@ -5,7 +5,8 @@
 
 'full' extracts the per-launch DRAM traffic, duration, throughput and pipe
 utilisation of each captured kernel and (with N) updates
-profiles/sweep_traffic.json, which bench.py reports as roofline.traffic.
+profiles/k_sweep2b_traffic.json (PLANES_PER_LAUNCH=p for a chunk launch of p
+planes), which bench.py reports as roofline.traffic / dram_bytes_per_site_update.
 'launches' aggregates a gpu__time_duration launch list per kernel name.
 """
 
@@ -101,10 +102,17 @@ def full(rep, label, n=None):
                 tr = json.load(f)
         except Exception:
             tr = {}
-        tr[str(n)] = {"dram_bytes_per_launch": first["dram_bytes_per_launch"],
-                      "duration_s": first.get("gpu__time_duration.sum"),
+        n = int(n)
+        planes = int(os.environ.get("PLANES_PER_LAUNCH", n))   # chunk launches: planes each
+        dram = first["dram_bytes_per_launch"]
+        inst = first.get("smsp__inst_executed.sum")
+        upd = (2 if kname == "k_sweep2b" else 1) * planes * n * n
+        tr[str(n)] = {"dram_bytes_per_pass": dram * n / planes, "dram_bytes_per_launch": dram,
+                      "planes_per_launch": planes,
+                      "thread_instructions_per_site_update": inst * 32 / upd if inst else None,
+                      "duration_s_per_launch": first.get("gpu__time_duration.sum"),
                       "kernel": first["kernel"], "source": f"profiles/ncu_{label}.json",
-                      "algorithmic_bytes": 24 * int(n) ** 3}
+                      "algorithmic_bytes_per_pass": 24 * n ** 3}
         with open(tpath, "w") as f:
             json.dump(tr, f, indent=1)
         print(tpath)
