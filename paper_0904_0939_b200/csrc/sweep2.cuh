@@ -2,6 +2,7 @@
 // Part of the single translation unit csrc/psigpu.cu (included there, inside its
 // anonymous namespace; the host engine instantiates the templates).
 #pragma once
+#include <type_traits>
 
 // ------------------------------------------------------------------
 // two sweeps per pass (temporal blocking, k_sweep2b): plain steps s, s+1 of
@@ -332,9 +333,11 @@ __device__ __forceinline__ void t2b_rows_item(const SweepArgs& args, const T2Ite
   double2 a0 = q0, a1 = q0, a2 = q0, f0 = q0, f1 = q0, f2 = q0;
   const int pend = I.z1 + 2;
   int p = I.z0 - 1;
+  // DO2: step 2 runs on this plane (false for an item's first two planes,
+  // which the loop below peels, so the steady loop carries no per-plane test)
   auto plane = [&](const double2& cp, const double2& cc, double2& cn, double2& qw,
                    const double2& qm, const double2& qmm, double2& aw, double2& fw,
-                   const double2& am, const double2& fm) {
+                   const double2& am, const double2& fm, auto do2) {
     mbar_wait_if(okf, nx.bar, nx.ph);   // probed one plane earlier
     // all warps' psi' of plane g-1, needed by step 2 below: probe now (ahead
     // of the shared loads, which the compiler keeps in order)
@@ -366,7 +369,7 @@ __device__ __forceinline__ void t2b_rows_item(const SweepArgs& args, const T2Ite
     // (the kernel's first plane waits on a pre-completed phase; no item
     // stores or computes step 2 in its first two planes)
     mbar_wait_if(okr, rg.br, rg.rph);
-    if (STEP2 && p > I.z0) {   // plane p-1 >= z0: an output plane of this item
+    if (STEP2 && decltype(do2)::value) {   // plane p-1 >= z0: an output plane of this item
       const uint32_t rq = base + ROFF + rg.rr;
       const double2 rjm = lds2_u(rq - BOXW * 8);
       const double2 rjp = lds2_u(rq + BOXW * 8);
@@ -404,12 +407,18 @@ __device__ __forceinline__ void t2b_rows_item(const SweepArgs& args, const T2Ite
     rg.next(rf0);
     ++p;
   };
+  using no2 = std::false_type;
+  using yes2 = std::true_type;
+  // planes z0-1 and z0 (step 1 only), then the steady 3-plane rotation from
+  // its third phase; an item has z1 - z0 + 3 >= 3 planes
+  plane(c_a, c_b, c_c, q0, q2, q1, a0, f0, a2, f2, no2{});
+  plane(c_b, c_c, c_a, q1, q0, q2, a1, f1, a0, f0, no2{});
   for (;;) {
-    plane(c_a, c_b, c_c, q0, q2, q1, a0, f0, a2, f2);
+    plane(c_c, c_a, c_b, q2, q1, q0, a2, f2, a1, f1, yes2{});
     if (p == pend) break;
-    plane(c_b, c_c, c_a, q1, q0, q2, a1, f1, a0, f0);
+    plane(c_a, c_b, c_c, q0, q2, q1, a0, f0, a2, f2, yes2{});
     if (p == pend) break;
-    plane(c_c, c_a, c_b, q2, q1, q0, a2, f2, a1, f1);
+    plane(c_b, c_c, c_a, q1, q0, q2, a1, f1, a0, f0, yes2{});
     if (p == pend) break;
   }
   g += (uint32_t)(pend - (I.z0 - 1));

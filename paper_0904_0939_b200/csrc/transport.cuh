@@ -517,6 +517,17 @@ int run_loop(std::vector<psg_slab*>& sl, Transport* tr, const psg_run_params* p,
         t += run - 1;
         continue;
       }
+      if (whole && run >= 3 && t3_ok(s0)) {
+        // triples of plain steps: three sweeps per pass over HBM (the rest as a pair / single)
+        const int64_t triples = run / 3;
+        for (int64_t q = 0; q < triples; ++q) {
+          NvtxRange nv("psg:pass3");
+          rc = do_sweep3(s0);
+          if (rc) return rc;
+        }
+        t += 3 * triples - 1;
+        continue;
+      }
       if (run >= 2) {
         // pairs of plain steps: two sweeps per pass over HBM
         const int64_t pairs = run / 2;

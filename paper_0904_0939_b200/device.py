@@ -76,7 +76,7 @@ def slab_field_bytes(n: int, w: int, single_buffer: bool = False, chunk: int = 0
     plane = (n + 2) * (((n + 5) + 3) // 4 * 4) * 8
     if single_buffer:
         c = min(chunk, w) if chunk > 0 else max(1, (w + 7) // 8)
-        return ((w + 4) + c + 2 + (w + 2)) * plane
+        return ((w + 4) + c + 3 + (w + 2)) * plane
     return (2 * (w + 4) + (w + 2)) * plane
 
 

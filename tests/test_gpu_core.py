@@ -41,6 +41,62 @@ def test_sweep_bitwise(gpu_lib, n):
     assert np.array_equal(got, want)
 
 
+@pytest.mark.parametrize("n,steps,every", [(16, 40, 0), (24, 37, 10), (40, 50, 20), (64, 61, 0),
+                                           (100, 47, 15), (130, 33, 0), (256, 22, 11)])
+def test_three_sweep_pass_matches_single_steps(gpu_lib, n, steps, every):
+    """Three sweeps per HBM pass (k_sweep3: two shared-memory rings of psi' and
+    psi'' planes) gives the bits of one launch per sweep, with norm / measure
+    steps cutting the runs and lattice sizes that leave partial tiles."""
+    spec = LatticeSpec(N=n, a=0.3, m=1.0, dtau=0.3 * 0.3 / 4.0)
+    rng = np.random.default_rng(n + 3)
+    ext = n + 2
+    psi0 = np.zeros((ext,) * 3)
+    psi0[1:-1, 1:-1, 1:-1] = rng.uniform(-0.5, 0.5, (n, n, n))
+    v = np.zeros((ext,) * 3)
+    v[1:-1, 1:-1, 1:-1] = rng.uniform(-1.0, 3.0, (n, n, n))
+    out = []
+    for mode in ("single", "t3"):
+        with Slab(spec) as s:
+            s.set_option(12, 0)
+            if mode == "single":
+                s.set_temporal(False)
+            else:
+                s.set_option(14, 1)
+            s.set_field(psi0)
+            s.set_potential(v)
+            idx, sums, status = s.run(steps, measure_every=every, norm_every=every)
+            out.append((s.get_field(), sums, s.launches()))
+    assert np.array_equal(out[0][0], out[1][0])
+    assert np.array_equal(out[0][1], out[1][1])
+    assert out[1][2] < out[0][2]
+
+
+@pytest.mark.parametrize("n,chunk", [(40, 1), (40, 5), (64, 17), (96, 0)])
+def test_three_sweep_pass_single_buffer(gpu_lib, n, chunk):
+    """k_sweep3 over the chunks of a single-buffer slab (buffers offset by
+    chunk + 3 planes) equals the two-buffer three-sweep run and the oracle."""
+    spec = LatticeSpec(N=n, a=0.3, m=1.0, dtau=0.3 * 0.3 / 4.0)
+    rng = np.random.default_rng(n + 11)
+    ext = n + 2
+    psi0 = np.zeros((ext,) * 3)
+    psi0[1:-1, 1:-1, 1:-1] = rng.uniform(-0.5, 0.5, (n, n, n))
+    v = np.zeros((ext,) * 3)
+    v[1:-1, 1:-1, 1:-1] = rng.uniform(-1.0, 3.0, (n, n, n))
+    want = psi0.copy()
+    for _ in range(9):
+        o = want.copy()
+        O.stencil_update_v(want, v, spec.dtau, spec.m, spec.a, o, 1, n)
+        want = o
+    for single in (False, True):
+        with Slab(spec, single_buffer=single, chunk=chunk if single else 0) as s:
+            s.set_option(12, 0)
+            s.set_option(14, 1)
+            s.set_field(psi0)
+            s.set_potential(v)
+            s.run(9, 0, 0)
+            assert np.array_equal(s.get_field(), want), (single, chunk)
+
+
 @pytest.mark.parametrize("n", [16, 32, 48, 64])
 def test_small_lattice_persistent_sweeps_bitwise(gpu_lib, n):
     """k_small (one persistent launch for a run of plain sweeps of a small

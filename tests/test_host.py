@@ -256,9 +256,9 @@ def test_slab_field_bytes_c5_sizes():
     assert slab_field_bytes(2048, 2048) == (2 * 2052 + 2050) * plane
     assert slab_field_bytes(2048, 2048) > 183e9 * 1.1
     one = slab_field_bytes(2048, 2048, single_buffer=True)
-    assert one == (2052 + 256 + 2 + 2050) * plane
+    assert one == (2052 + 256 + 3 + 2050) * plane
     assert 140e9 < one < 150e9
-    assert slab_field_bytes(64, 64, True, 8) == ((64 + 4) + 10 + 66) * 66 * 72 * 8
+    assert slab_field_bytes(64, 64, True, 8) == ((64 + 4) + 11 + 66) * 66 * 72 * 8
     # 2 GPUs at 2048^3: three fields of a 1024-plane slab
     assert slab_field_bytes(2048, 1024) < 110e9
 
