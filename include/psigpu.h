@@ -418,7 +418,9 @@ int psg_tune(psg_slab* s, int blocks_per_sm, int zchunk, int stages);
  * separate copy; needs W >= 4 and peer access, else the copies are used
  * (bitwise unchanged), 12 = persistent brick kernel (k_small) for runs of plain
  * sweeps of a whole lattice with N <= 64, N % 16 == 0 (default 1; bitwise
- * unchanged). */
+ * unchanged), 14 = three sweeps per HBM pass (k_sweep3) for runs of plain
+ * sweeps of a whole lattice (default 0: measured slower than the two-sweep
+ * pass; bitwise unchanged). */
 int psg_set_option(psg_slab* s, int option, int value);
 
 /* Enable / disable two sweeps per HBM pass (temporal blocking) for pairs of
