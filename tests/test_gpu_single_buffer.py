@@ -136,7 +136,7 @@ def test_single_buffer_memory_and_limits(gpu_lib):
     with Slab(spec) as two, Slab(spec, single_buffer=True, chunk=8) as one:
         ps = one.plane_stride * 8
         assert two.field_bytes == (2 * (n + 4) + (n + 2)) * ps
-        assert one.field_bytes == ((n + 4) + 10 + (n + 2)) * ps
+        assert one.field_bytes == ((n + 4) + 11 + (n + 2)) * ps   # buffers offset by chunk + 3 planes
         assert two.field_bytes == slab_field_bytes(n, n)
         assert one.field_bytes == slab_field_bytes(n, n, True, 8)
         assert not two.single_buffer and one.single_buffer    # auto: two buffers fit
