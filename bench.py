@@ -496,6 +496,11 @@ def time_pass(slab, st, npass, reserve_sms=0):
     return ea.elapsed_time(eb) * 1e-3 / npass
 
 
+def small_lattice(n) -> bool:
+    """Runs of plain sweeps go through k_small (psigpu.cu small_ok: N <= 64, N % 16 == 0)."""
+    return n <= 64 and n % 16 == 0
+
+
 def roofline(n, pass_s, glups, per_pass_launches, sites_per_gpu=None):
     peak, peak_kind = hbm_peak()
     sites = sites_per_gpu or n ** 3
@@ -505,8 +510,11 @@ def roofline(n, pass_s, glups, per_pass_launches, sites_per_gpu=None):
            "frac_basis": "24 B/site of HBM per two-sweep pass (psi read, V read, psi write) / "
                          "pass duration / measured copy bandwidth",
            "frac_per_update_basis": BYTES_PER_SITE * glups / peak,
-           "kernel": "k_sweep2b (two fp64 7-point sweeps per HBM pass, TMA z-march)"
-                     + (f", {per_pass_launches} launches per pass" if per_pass_launches > 1 else ""),
+           "kernel": ("k_small (persistent brick kernel: a run of plain sweeps in one launch; "
+                      "'pass' = two of its sweeps)" if small_lattice(n) and sites_per_gpu is None
+                      else "k_sweep2b (two fp64 7-point sweeps per HBM pass, TMA z-march)"
+                      + (f", {per_pass_launches} launches per pass" if per_pass_launches > 1
+                         else "")),
            "pass_us": pass_s * 1e6, "peak_source": peak_kind,
            "algorithmic_bytes_per_pass": BYTES_PER_SITE * sites,
            "site_updates_per_pass": 2 * sites, "traffic": None}
