@@ -17,10 +17,14 @@
 // steps 2 and 3 on the rows of their regions), ring warps for the four side
 // columns k0-2, k0-1, k0+64, k0+65 (one site per lane; step 2 on k0-1 and
 // k0+64), one TMA producer warp.  psi' and psi'' planes go through two rings
-// of 4 shared-memory slots, each written in iteration g (slot g % 4) and read
-// in iteration g+1, ordered by per-slot mbarriers exactly like k_sweep2b's
-// ring (a slot is rewritten at g+4, after its writer has waited on the
-// iteration-(g+2) barrier, i.e. after every warp finished iteration g+1).
+// of 4 shared-memory slots, both written in iteration g (slot g % 4) and read
+// in iteration g+1; ONE per-slot mbarrier covers both: a warp arrives at the
+// end of iteration g (psi'(p) and psi''(p-1) stored) and waits, before its
+// steps 2 and 3 of iteration g+1, for everyone's iteration-g arrival.  A slot
+// is rewritten at g+4, after its writer has waited on the iteration-(g+2)
+// barrier, i.e. after every warp finished iteration g+2 (its reads were in
+// g+1).  One barrier round per plane, like k_sweep2b (a first version with a
+// round per ring issued at 37 %).
 // A and C are formed once per site in step 1 and kept in registers for
 // steps 2 and 3 (three rotating sets).  Per-site arithmetic is k_sweep's, so
 // the result is bitwise three k_sweep launches (tests/test_gpu_core.py).
@@ -51,8 +55,8 @@ struct T3Cfg {
   using G = T3Geo<TB>;
   static constexpr int R1_OFF = NST * G::STAGE;
   static constexpr int R2_OFF = R1_OFF + 4 * G::R1;
-  static constexpr int BAR_OFF = R2_OFF + 4 * G::R2;    // full[NST], empty[NST], r1[4], r2[4]
-  static constexpr int SMEM = BAR_OFF + (2 * NST + 8) * 8;
+  static constexpr int BAR_OFF = R2_OFF + 4 * G::R2;    // full[NST], empty[NST], ring[4]
+  static constexpr int SMEM = BAR_OFF + (2 * NST + 4) * 8;
 };
 
 template <int TB>
@@ -116,7 +120,6 @@ __device__ __forceinline__ void t3_rows_item(const SweepArgs& args, const T2Item
   const uint32_t r1_row = C::R1_OFF + (uint32_t)w * RW8 + col;
   const uint32_t r2_row = C::R2_OFF + (uint32_t)(w - 1) * RW8 + col;   // w >= 1 for S2
   const uint32_t r1bar = sm0 + C::BAR_OFF + 2 * S * 8;
-  const uint32_t r2bar = r1bar + 4 * 8;
   const bool in_j = (unsigned)(j - 1) < (unsigned)n;
   const bool in0 = in_j & (k <= n);
   const bool in1 = in_j & (k + 1 <= n);
@@ -174,12 +177,11 @@ __device__ __forceinline__ void t3_rows_item(const SweepArgs& args, const T2Item
     const uint32_t s1 = (g & 3u);
     sts2_u(sm0 + r1_row + s1 * G::R1, q[P0]);
     mbar_arrive_u(cur_bar + S * 8);     // stage of plane p consumed
-    mbar_arrive_u(r1bar + s1 * 8);      // psi'(p) published
     cur_sb = sy.sb;
     cur_bar = sy.sbar;
     sy.next();
-    // step 2 on plane p-1 from psi'(p-1) (published in iteration g-1)
-    const bool ok2 = mbar_test_u(r2bar + sr * 8, rph);
+    // steps 2 and 3 read what every warp published in iteration g-1:
+    // psi'(p-1) (ring 1) and psi''(p-2) (ring 2) -- one barrier round per plane
     mbar_wait_if(ok1, r1bar + sr * 8, rph);
     if (DO2) {
       const uint32_t rq = sm0 + r1_row + sr * G::R1;
@@ -199,9 +201,7 @@ __device__ __forceinline__ void t3_rows_item(const SweepArgs& args, const T2Item
       }
       sts2_u(sm0 + r2_row + s1 * G::R2, r[PM]);
     }
-    mbar_arrive_u(r2bar + s1 * 8);      // psi''(p-1) published (slot of iteration g)
     // step 3 on plane p-2 from psi''(p-2) (published in iteration g-1)
-    mbar_wait_if(ok2, r2bar + sr * 8, rph);
     if (DO3) {
       const uint32_t rr = sm0 + r2_row + sr * G::R2;
       const double2 sjm = lds2_u(rr - RW8);
@@ -219,6 +219,7 @@ __device__ __forceinline__ void t3_rows_item(const SweepArgs& args, const T2Item
       }
       doff += pstride;
     }
+    mbar_arrive_u(r1bar + s1 * 8);      // psi'(p) and psi''(p-1) published
     ++g;
     ++p;
   };
@@ -270,7 +271,6 @@ __device__ __forceinline__ void t3_ring_item(const SweepArgs& args, const T2Item
   const uint32_t r1_row = C::R1_OFF + (uint32_t)rr0 * RW8 + colb;
   const uint32_t r2_row = C::R2_OFF + (uint32_t)(rr0 > 0 ? rr0 - 1 : 0) * RW8 + colb;
   const uint32_t r1bar = sm0 + C::BAR_OFF + 2 * S * 8;
-  const uint32_t r2bar = r1bar + 4 * 8;
   const bool in_jk = active & ((unsigned)(j - 1) < (unsigned)n) & ((unsigned)(k - 1) < (unsigned)n);
   double c[3], q[3], av[3], fv[3];
   mbar_wait_u(sy.sbar, sy.sph);
@@ -307,11 +307,9 @@ __device__ __forceinline__ void t3_ring_item(const SweepArgs& args, const T2Item
     const uint32_t s1 = (g & 3u);
     if (active) sts1_u(sm0 + r1_row + s1 * G::R1, q[P0]);
     mbar_arrive_u(cur_bar + S * 8);
-    mbar_arrive_u(r1bar + s1 * 8);
     cur_sb = sy.sb;
     cur_bar = sy.sbar;
     sy.next();
-    const bool ok2 = mbar_test_u(r2bar + sr * 8, rph);
     mbar_wait_if(ok1, r1bar + sr * 8, rph);
     if (D2 && do2) {
       const uint32_t rq = sm0 + r1_row + sr * G::R1;
@@ -324,8 +322,7 @@ __device__ __forceinline__ void t3_ring_item(const SweepArgs& args, const T2Item
       if (MASK) ov = (((unsigned)(p - 2) < (unsigned)n) & in_jk) ? o : q[PM];
       sts1_u(sm0 + r2_row + s1 * G::R2, ov);
     }
-    mbar_arrive_u(r2bar + s1 * 8);
-    mbar_wait_if(ok2, r2bar + sr * 8, rph);   // keeps this warp in the ring lock-step (no step 3)
+    mbar_arrive_u(r1bar + s1 * 8);      // psi'(p) and psi''(p-1) published
     ++g;
     ++p;
   };
@@ -358,7 +355,6 @@ __global__ void __launch_bounds__(T3Geo<TB>::THREADS, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
   uint64_t* empty = full + S;
   uint64_t* r1 = empty + S;
-  uint64_t* r2 = r1 + 4;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -366,20 +362,14 @@ __global__ void __launch_bounds__(T3Geo<TB>::THREADS, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], G::CW * 32);
     }
-    for (int i = 0; i < 4; ++i) {
-      mbar_init(&r1[i], G::CW * 32);
-      mbar_init(&r2[i], G::CW * 32);
-    }
+    for (int i = 0; i < 4; ++i) mbar_init(&r1[i], G::CW * 32);
     fence_barrier_init();
   }
   __syncthreads();
   // both rings count iterations from 4: every consumer lane completes phase 0
   // of each slot once, so the first iterations' waits are already satisfied
   if (warp < G::CW) {
-    for (int i = 0; i < 4; ++i) {
-      mbar_arrive(&r1[i]);
-      mbar_arrive(&r2[i]);
-    }
+    for (int i = 0; i < 4; ++i) mbar_arrive(&r1[i]);
   }
   pdl_launch_dependents();
   pdl_wait();
