@@ -129,6 +129,9 @@ __device__ double block_pairwise(const double* a, int n, CombineSmem& sm) {
 constexpr int S_E = 4, S_NORM2 = 5, S_RRMS = 6, S_N2 = 7, S_FACTOR = 8, S_STATUS = 9, S_ONE = 11;
 constexpr int NSCAL = 16;
 
+__device__ void combine_scalars(const double* tot, unsigned qmask, double a3, double* scal,
+                                double* hist_rec, const int* bad);
+
 // cross-plane combine exactly like observables.combine_plane_sums (np.sum) and
 // the scalars of evolve._record_from_sums / SweepBuffers.renormalize
 __device__ void combine_body(const double* plane_sums, int n, unsigned qmask, double a3,
@@ -145,7 +148,18 @@ __device__ void combine_body(const double* plane_sums, int n, unsigned qmask, do
     }
     tot[q] = block_pairwise(a, n, sm);
   }
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0) combine_scalars(tot, qmask, a3, scal, hist_rec, bad);
+  // copy the measured plane sums into the history record
+  if (hist_rec && (qmask & 7u) == 7u) {
+    for (int i = threadIdx.x; i < 3 * n; i += blockDim.x) hist_rec[2 + i] = __ldcg(plane_sums + i);
+  }
+}
+
+// the scalars of evolve._record_from_sums / SweepBuffers.renormalize from the
+// totals (thread 0 of the combining block)
+__device__ void combine_scalars(const double* tot, unsigned qmask, double a3, double* scal,
+                                double* hist_rec, const int* bad) {
+  {
     for (int q = 0; q < NQ; ++q)
       if (qmask & (1u << q)) scal[q] = tot[q];
     double status = scal[S_STATUS];
@@ -173,10 +187,6 @@ __device__ void combine_body(const double* plane_sums, int n, unsigned qmask, do
     }
     if (bad && __ldcg(bad) && status == 0.0) status = 4.0;
     scal[S_STATUS] = status;
-  }
-  // copy the measured plane sums into the history record
-  if (hist_rec && (qmask & 7u) == 7u) {
-    for (int i = threadIdx.x; i < 3 * n; i += blockDim.x) hist_rec[2 + i] = __ldcg(plane_sums + i);
   }
 }
 
@@ -260,5 +270,44 @@ __global__ void __launch_bounds__(NT_THREADS)
     }
     if (bad && __ldcg(bad) && status == 0.0) status = 4.0;
     scal[S_STATUS] = status;
+  }
+}
+
+// Small whole lattices (n <= 128): tile partials -> plane sums -> combine in ONE
+// block (no cross-block counter, no recursion): warp w reduces planes w, w+8,
+// ... exactly like k_plane_reduce, then warp q's lane 0 forms quantity q's
+// np.sum (0.0 + one pairwise leaf, numpy's order for n <= 128) -- bitwise the
+// multi-block path.  Measured: the multi-block reduce + combine takes 9-13 us
+// at 64^3 (profiles/ncu_r02_c1_small.json), most of a norm / measure step.
+constexpr int RS_MAX_N = 128;
+__global__ void __launch_bounds__(32 * RED_WARPS)
+    k_reduce_small(const double* __restrict__ part, double* plane_sums, unsigned qmask,
+                   long long qstride, int tiles, int z_lo, int z_hi, int x_off, int n, double a3,
+                   double* scal, double* hist_rec, const int* bad) {
+  __shared__ double ps[NQ][RS_MAX_N];
+  __shared__ double tot[NQ];
+  pdl_launch_dependents();
+  pdl_wait();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int p = z_lo + warp; p <= z_hi; p += RED_WARPS) {
+    const int gplane = x_off + p - 1;
+    for (int q = 0; q < NQ; ++q) {
+      if (!(qmask & (1u << q))) continue;
+      const double* src = part + (size_t)q * qstride + (size_t)p * tiles;
+      double acc = 0.0;
+      for (int t = lane; t < tiles; t += 32) acc = __dadd_rn(acc, src[t]);
+      acc = warp_sum(acc);
+      if (lane == 0 && gplane >= 0 && gplane < n) {
+        plane_sums[(size_t)q * n + gplane] = acc;
+        ps[q][gplane] = acc;
+      }
+    }
+  }
+  __syncthreads();
+  if (lane == 0 && warp < NQ && (qmask & (1u << warp))) tot[warp] = __dadd_rn(0.0, pw_leaf(ps[warp], n));
+  __syncthreads();
+  if (threadIdx.x == 0) combine_scalars(tot, qmask, a3, scal, hist_rec, bad);
+  if (hist_rec && (qmask & 7u) == 7u) {
+    for (int i = threadIdx.x; i < 3 * n; i += blockDim.x) hist_rec[2 + i] = ps[i / n][i % n];
   }
 }

@@ -145,3 +145,256 @@ __global__ void __launch_bounds__(SB_THREADS, 1) k_small(const SmallArgs a) {
 #pragma unroll
   for (int i = 0; i < SB_I; ++i) a.out[at(i0 + i, j0 + tj, k0 + tk)] = c[i];
 }
+
+// ---------------------------------------------------------------------------
+// k_small2: the same bricks with TWO-deep halos -- one face exchange per two
+// sweeps (the exchange, ~2 us through L2, is what k_small's sweeps cost; its
+// compute is 0.5 us).  Per pair: sweep A on the brick and its face ring (the
+// sites one step outside the brick along one axis), sweep B on the brick from
+// sweep A's values.  Sweep A at a face-ring site reads the halo two deep along
+// its axis and the EDGE sites one step out along two axes, which belong to the
+// 12 diagonal bricks; they are read from those bricks' published faces (an
+// edge line lies in a face layer).  A run of odd length ends with one sweep
+// from the one-deep halo.  Bitwise k_sweep's per-site arithmetic.
+constexpr int SB2_FACE = 4 * SB_J * SB_K + 8 * SB_I * SB_K;   // two layers per face
+constexpr int S2_E = SB_I + 4, S2_J = SB_J + 4, S2_K = SB_K + 4;   // S0 box (halo 2)
+constexpr int SA_E = SB_I + 2, SA_J = SB_J + 2, SA_K = SB_K + 2;   // sweep-A box (halo 1)
+constexpr int SB2_RING = 2 * SB_J * SB_K + 4 * SB_I * SB_K;       // face-ring sites
+constexpr int SB2_SMEM = (S2_E * S2_J * S2_K + SA_E * SA_J * SA_K + 2 * SB2_RING) * 8;
+
+template <bool FASTC>
+__global__ void __launch_bounds__(SB_THREADS, 1) k_small2(const SmallArgs a) {
+  extern __shared__ __align__(16) double sm2[];
+  double* S0 = sm2;                                   // [S2_E][S2_J][S2_K], site (i,j,k) at (i+2, j+2, k+2)
+  double* SA = S0 + S2_E * S2_J * S2_K;               // [SA_E][SA_J][SA_K], site at (i+1, j+1, k+1)
+  double* RA = SA + SA_E * SA_J * SA_K;               // face-ring A coefficients [SB2_RING]
+  double* RC = RA + SB2_RING;                         // face-ring C coefficients
+  auto s0 = [&](int i, int j, int k) -> double& { return S0[((i + 2) * S2_J + (j + 2)) * S2_K + (k + 2)]; };
+  auto sa = [&](int i, int j, int k) -> double& { return SA[((i + 1) * SA_J + (j + 1)) * SA_K + (k + 1)]; };
+  const int b = blockIdx.x;
+  const int bk = b % a.nbk;
+  const int bj = (b / a.nbk) % a.nbj;
+  const int bi = b / (a.nbk * a.nbj);
+  const int t = threadIdx.x;
+  const int tk = t % SB_K, tj = t / SB_K;
+  const int i0 = 1 + bi * SB_I, j0 = 1 + bj * SB_J, k0 = 1 + bk * SB_K;
+  const int n = a.n;
+  const long long ps = a.plane_stride;
+  auto at = [&](int i, int j, int k) { return (long long)i * ps + (long long)j * a.pitch + k + COL_OFF; };
+  auto inlat = [&](int gi, int gj, int gk) {
+    return ((unsigned)(gi - 1) < (unsigned)n) & ((unsigned)(gj - 1) < (unsigned)n) &
+           ((unsigned)(gk - 1) < (unsigned)n);
+  };
+  pdl_wait();
+  // S0: the brick with a two-deep halo box from the input field (outside the
+  // lattice: padding zeros, or beyond the allocation's planes: zero)
+  for (int q = t; q < S2_E * S2_J * S2_K; q += SB_THREADS) {
+    const int kk = q % S2_K, r = q / S2_K;
+    const int jj = r % S2_J, ii = r / S2_J;
+    const int gi = i0 - 2 + ii, gj = j0 - 2 + jj, gk = k0 - 2 + kk;
+    const bool in_box = (gi >= 0) & (gi <= n + 1) & (gj >= 0) & (gj <= n + 1) & (gk >= 0) & (gk <= n + 1);
+    S0[q] = in_box ? a.in[at(gi, gj, gk)] : 0.0;
+  }
+  // face-ring site q of this thread's four (two i-face sites, one j-face, one k-face)
+  // -> local coordinates; ring index layout: i-lo 0..255, i-hi 256.., j-lo 512, j-hi 640,
+  // k-lo 768, k-hi 896
+  int ri[4], rj[4], rk[4], rx[4];
+  {
+    ri[0] = -1; rj[0] = tj; rk[0] = tk; rx[0] = t;
+    ri[1] = SB_I; rj[1] = tj; rk[1] = tk; rx[1] = 256 + t;
+    const int u = t & 127, hi = t >> 7;
+    ri[2] = u / SB_K; rj[2] = hi ? SB_J : -1; rk[2] = u % SB_K; rx[2] = 512 + 128 * hi + u;
+    ri[3] = u / SB_J; rj[3] = u % SB_J; rk[3] = hi ? SB_K : -1; rx[3] = 768 + 128 * hi + u;
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int gi = i0 + ri[q], gj = j0 + rj[q], gk = k0 + rk[q];
+    double A = 0.0, C = 0.0;
+    if (inlat(gi, gj, gk)) coef_pair(a.v[at(gi, gj, gk)], a.h, a.c0, A, C);
+    RA[rx[q]] = A;
+    RC[rx[q]] = C;
+  }
+  double A[SB_I], C[SB_I], c[SB_I];
+#pragma unroll
+  for (int i = 0; i < SB_I; ++i) coef1<FASTC>(a.v[at(i0 + i, j0 + tj, k0 + tk)], a.h, a.c0, A[i], C[i]);
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < SB_I; ++i) c[i] = s0(i, tj, tk);
+  bool rin[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) rin[q] = inlat(i0 + ri[q], j0 + rj[q], k0 + rk[q]);
+  const int nbs = a.nbi * a.nbj * a.nbk;
+  auto bid = [&](int di, int dj, int dk) {   // neighbour brick or -1
+    const int xi = bi + di, xj = bj + dj, xk = bk + dk;
+    if (xi < 0 || xi >= a.nbi || xj < 0 || xj >= a.nbj || xk < 0 || xk >= a.nbk) return -1;
+    return (xi * a.nbj + xj) * a.nbk + xk;
+  };
+  // face record of a brick (two layers per face): i-lo layers (0,1) [2][J][K],
+  // i-hi layers (I-2, I-1), j-lo (0,1) [2][I][K], j-hi, k-lo (0,1) [2][I][J], k-hi
+  constexpr int F_ILO = 0, F_IHI = 2 * SB_J * SB_K, F_JLO = 4 * SB_J * SB_K;
+  constexpr int F_JHI = F_JLO + 2 * SB_I * SB_K, F_KLO = F_JHI + 2 * SB_I * SB_K;
+  constexpr int F_KHI = F_KLO + 2 * SB_I * SB_J;
+  int s = 0;
+  while (s < a.steps) {
+    if (a.steps - s >= 2) {
+      // ---- sweep A: brick (registers) and face ring ----
+      double av[SB_I];
+#pragma unroll
+      for (int i = 0; i < SB_I; ++i) {
+        const double im = i == 0 ? s0(-1, tj, tk) : c[i - 1];
+        const double ip = i == SB_I - 1 ? s0(SB_I, tj, tk) : c[i + 1];
+        av[i] = upd(A[i], C[i], c[i], im, ip, s0(i, tj - 1, tk), s0(i, tj + 1, tk),
+                    s0(i, tj, tk - 1), s0(i, tj, tk + 1));
+        sa(i, tj, tk) = av[i];
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int i = ri[q], j = rj[q], k = rk[q];
+        const double cv = s0(i, j, k);
+        const double u = upd(RA[rx[q]], RC[rx[q]], cv, s0(i - 1, j, k), s0(i + 1, j, k),
+                             s0(i, j - 1, k), s0(i, j + 1, k), s0(i, j, k - 1), s0(i, j, k + 1));
+        sa(i, j, k) = rin[q] ? u : cv;
+      }
+      __syncthreads();
+      // ---- sweep B: the brick ----
+#pragma unroll
+      for (int i = 0; i < SB_I; ++i) {
+        const double im = i == 0 ? sa(-1, tj, tk) : av[i - 1];
+        const double ip = i == SB_I - 1 ? sa(SB_I, tj, tk) : av[i + 1];
+        c[i] = upd(A[i], C[i], av[i], im, ip, sa(i, tj - 1, tk), sa(i, tj + 1, tk),
+                   sa(i, tj, tk - 1), sa(i, tj, tk + 1));
+      }
+      s += 2;
+    } else {
+      // ---- one sweep from the one-deep halo (the last of an odd run) ----
+      double nv[SB_I];
+#pragma unroll
+      for (int i = 0; i < SB_I; ++i) {
+        const double im = i == 0 ? s0(-1, tj, tk) : c[i - 1];
+        const double ip = i == SB_I - 1 ? s0(SB_I, tj, tk) : c[i + 1];
+        nv[i] = upd(A[i], C[i], c[i], im, ip, s0(i, tj - 1, tk), s0(i, tj + 1, tk),
+                    s0(i, tj, tk - 1), s0(i, tj, tk + 1));
+      }
+#pragma unroll
+      for (int i = 0; i < SB_I; ++i) c[i] = nv[i];
+      s += 1;
+    }
+    if (s >= a.steps) break;
+    __syncthreads();   // every read of S0 / SA for this pair is done
+#pragma unroll
+    for (int i = 0; i < SB_I; ++i) s0(i, tj, tk) = c[i];
+    // ---- publish the two-layer faces of the new state (parity by pair) ----
+    const uint32_t tag = (uint32_t)(a.base + (unsigned long long)s);
+    const int par = (s >> 1) & 1;
+    unsigned long long* f = a.faces + ((size_t)par * nbs + b) * (2 * SB2_FACE);
+    put_tagged(f + 2 * (F_ILO + (0 * SB_J + tj) * SB_K + tk), c[0], tag);
+    put_tagged(f + 2 * (F_ILO + (1 * SB_J + tj) * SB_K + tk), c[1], tag);
+    put_tagged(f + 2 * (F_IHI + (0 * SB_J + tj) * SB_K + tk), c[SB_I - 2], tag);
+    put_tagged(f + 2 * (F_IHI + (1 * SB_J + tj) * SB_K + tk), c[SB_I - 1], tag);
+#pragma unroll
+    for (int i = 0; i < SB_I; ++i) {
+      if (tj < 2) put_tagged(f + 2 * (F_JLO + (tj * SB_I + i) * SB_K + tk), c[i], tag);
+      if (tj >= SB_J - 2) put_tagged(f + 2 * (F_JHI + ((tj - (SB_J - 2)) * SB_I + i) * SB_K + tk), c[i], tag);
+      if (tk < 2) put_tagged(f + 2 * (F_KLO + (tk * SB_I + i) * SB_J + tj), c[i], tag);
+      if (tk >= SB_K - 2) put_tagged(f + 2 * (F_KHI + ((tk - (SB_K - 2)) * SB_I + i) * SB_J + tj), c[i], tag);
+    }
+    // ---- read the halo: faces two deep, the 12 edge lines one deep ----
+    // every load of this thread is issued before any tag is checked (one L2
+    // round trip for all of them), then only the values not yet tagged with
+    // this pair's sweep are loaded again
+    const unsigned long long* fs = a.faces + (size_t)par * nbs * (2 * SB2_FACE);
+    auto rec = [&](int q, int off) { return fs + (size_t)q * (2 * SB2_FACE) + 2 * off; };
+    // fixed slots (registers, no local memory): 0-3 i-faces, 4-5 j-faces,
+    // 6-7 k-faces, 8 an edge value
+    constexpr int MAXG = 9;
+    const unsigned long long* src[MAXG];
+    int dst[MAXG];
+    unsigned pend = 0;
+#pragma unroll
+    for (int g2 = 0; g2 < MAXG; ++g2) {
+      src[g2] = fs;
+      dst[g2] = 0;
+    }
+    auto want = [&](auto slot, int q, int off, int i, int j, int k) {
+      constexpr int G2 = decltype(slot)::value;
+      src[G2] = rec(q, off);
+      dst[G2] = ((i + 2) * S2_J + (j + 2)) * S2_K + (k + 2);
+      pend |= 1u << G2;
+    };
+    using Z0 = std::integral_constant<int, 0>;
+    using Z1 = std::integral_constant<int, 1>;
+    using Z2 = std::integral_constant<int, 2>;
+    using Z3 = std::integral_constant<int, 3>;
+    using Z4 = std::integral_constant<int, 4>;
+    using Z5 = std::integral_constant<int, 5>;
+    using Z6 = std::integral_constant<int, 6>;
+    using Z7 = std::integral_constant<int, 7>;
+    using Z8 = std::integral_constant<int, 8>;
+    {
+      const int qlo = bid(-1, 0, 0), qhi = bid(1, 0, 0);
+      if (qlo >= 0) {   // its layers I-2, I-1 -> my i = -2, -1
+        want(Z0{}, qlo, F_IHI + (0 * SB_J + tj) * SB_K + tk, -2, tj, tk);
+        want(Z1{}, qlo, F_IHI + (1 * SB_J + tj) * SB_K + tk, -1, tj, tk);
+      }
+      if (qhi >= 0) {   // its layers 0, 1 -> my i = I, I+1
+        want(Z2{}, qhi, F_ILO + (0 * SB_J + tj) * SB_K + tk, SB_I, tj, tk);
+        want(Z3{}, qhi, F_ILO + (1 * SB_J + tj) * SB_K + tk, SB_I + 1, tj, tk);
+      }
+    }
+    {
+      const int layer = t >> 7, u = t & 127, i = u / SB_K, k = u % SB_K;
+      const int qlo = bid(0, -1, 0), qhi = bid(0, 1, 0);
+      if (qlo >= 0) want(Z4{}, qlo, F_JHI + (layer * SB_I + i) * SB_K + k, i, layer - 2, k);
+      if (qhi >= 0) want(Z5{}, qhi, F_JLO + (layer * SB_I + i) * SB_K + k, i, SB_J + layer, k);
+      const int j = u % SB_J, ik = u / SB_J;
+      const int plo = bid(0, 0, -1), phi = bid(0, 0, 1);
+      if (plo >= 0) want(Z6{}, plo, F_KHI + (layer * SB_I + ik) * SB_J + j, ik, j, layer - 2);
+      if (phi >= 0) want(Z7{}, phi, F_KLO + (layer * SB_I + ik) * SB_J + j, ik, j, SB_K + layer);
+    }
+    if (t < 4 * SB_K) {   // edge lines along k: (i, j) corners
+      const int e = t / SB_K, k = t % SB_K;
+      const int di = (e & 1) ? 1 : -1, dj = (e & 2) ? 1 : -1;
+      const int q = bid(di, dj, 0);
+      if (q >= 0)   // neighbour's site (I-1 | 0, J-1 | 0, k): in its i-face layer
+        want(Z8{}, q, (di < 0 ? F_IHI + (1 * SB_J + (dj < 0 ? SB_J - 1 : 0)) * SB_K
+                        : F_ILO + (0 * SB_J + (dj < 0 ? SB_J - 1 : 0)) * SB_K) + k,
+             di < 0 ? -1 : SB_I, dj < 0 ? -1 : SB_J, k);
+    } else if (t < 8 * SB_K) {   // along j: (i, k) corners
+      const int u = t - 4 * SB_K, e = u / SB_J, j = u % SB_J;
+      const int di = (e & 1) ? 1 : -1, dk = (e & 2) ? 1 : -1;
+      const int q = bid(di, 0, dk);
+      if (q >= 0)
+        want(Z8{}, q, (di < 0 ? F_IHI + (1 * SB_J + j) * SB_K : F_ILO + (0 * SB_J + j) * SB_K) +
+                    (dk < 0 ? SB_K - 1 : 0),
+             di < 0 ? -1 : SB_I, j, dk < 0 ? -1 : SB_K);
+    } else if (t < 8 * SB_K + 4 * SB_I) {   // along i: (j, k) corners
+      const int u = t - 8 * SB_K, e = u / SB_I, i = u % SB_I;
+      const int dj = (e & 1) ? 1 : -1, dk = (e & 2) ? 1 : -1;
+      const int q = bid(0, dj, dk);
+      if (q >= 0)   // neighbour's site (i, J-1 | 0, K-1 | 0): in its j-face layer
+        want(Z8{}, q, dj < 0 ? F_JHI + (1 * SB_I + i) * SB_K + (dk < 0 ? SB_K - 1 : 0)
+                       : F_JLO + (0 * SB_I + i) * SB_K + (dk < 0 ? SB_K - 1 : 0),
+             i, dj < 0 ? -1 : SB_J, dk < 0 ? -1 : SB_K);
+    }
+    unsigned spins = 0;
+    while (pend) {
+      unsigned long long w0[MAXG], w1[MAXG];
+#pragma unroll
+      for (int g2 = 0; g2 < MAXG; ++g2)
+        if (pend & (1u << g2))
+          asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];"
+                       : "=l"(w0[g2]), "=l"(w1[g2]) : "l"(src[g2]) : "memory");
+#pragma unroll
+      for (int g2 = 0; g2 < MAXG; ++g2)
+        if ((pend & (1u << g2)) && (uint32_t)w0[g2] == tag && (uint32_t)w1[g2] == tag) {
+          S0[dst[g2]] = __longlong_as_double((long long)((w1[g2] & 0xffffffff00000000ull) | (w0[g2] >> 32)));
+          pend &= ~(1u << g2);
+        }
+      if (++spins > (1u << 30)) __trap();
+    }
+    __syncthreads();
+  }
+  pdl_launch_dependents();
+#pragma unroll
+  for (int i = 0; i < SB_I; ++i) a.out[at(i0 + i, j0 + tj, k0 + tk)] = c[i];
+}
