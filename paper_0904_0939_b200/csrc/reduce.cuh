@@ -280,7 +280,8 @@ __global__ void __launch_bounds__(NT_THREADS)
 // multi-block path.  Measured: the multi-block reduce + combine takes 9-13 us
 // at 64^3 (profiles/ncu_r02_c1_small.json), most of a norm / measure step.
 constexpr int RS_MAX_N = 128;
-__global__ void __launch_bounds__(32 * RED_WARPS)
+constexpr int RS_WARPS = 32;
+__global__ void __launch_bounds__(32 * RS_WARPS)
     k_reduce_small(const double* __restrict__ part, double* plane_sums, unsigned qmask,
                    long long qstride, int tiles, int z_lo, int z_hi, int x_off, int n, double a3,
                    double* scal, double* hist_rec, const int* bad) {
@@ -289,18 +290,22 @@ __global__ void __launch_bounds__(32 * RED_WARPS)
   pdl_launch_dependents();
   pdl_wait();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int p = z_lo + warp; p <= z_hi; p += RED_WARPS) {
+  // (quantity, plane) pairs spread over all 32 warps
+  int qs[NQ], nq = 0;
+  for (int q = 0; q < NQ; ++q)
+    if (qmask & (1u << q)) qs[nq++] = q;
+  const int np = z_hi - z_lo + 1;
+  for (int w = warp; w < nq * np; w += RS_WARPS) {
+    const int q = qs[w / np];
+    const int p = z_lo + w % np;
     const int gplane = x_off + p - 1;
-    for (int q = 0; q < NQ; ++q) {
-      if (!(qmask & (1u << q))) continue;
-      const double* src = part + (size_t)q * qstride + (size_t)p * tiles;
-      double acc = 0.0;
-      for (int t = lane; t < tiles; t += 32) acc = __dadd_rn(acc, src[t]);
-      acc = warp_sum(acc);
-      if (lane == 0 && gplane >= 0 && gplane < n) {
-        plane_sums[(size_t)q * n + gplane] = acc;
-        ps[q][gplane] = acc;
-      }
+    const double* src = part + (size_t)q * qstride + (size_t)p * tiles;
+    double acc = 0.0;
+    for (int t = lane; t < tiles; t += 32) acc = __dadd_rn(acc, src[t]);
+    acc = warp_sum(acc);
+    if (lane == 0 && gplane >= 0 && gplane < n) {
+      plane_sums[(size_t)q * n + gplane] = acc;
+      ps[q][gplane] = acc;
     }
   }
   __syncthreads();
@@ -308,6 +313,7 @@ __global__ void __launch_bounds__(32 * RED_WARPS)
   __syncthreads();
   if (threadIdx.x == 0) combine_scalars(tot, qmask, a3, scal, hist_rec, bad);
   if (hist_rec && (qmask & 7u) == 7u) {
-    for (int i = threadIdx.x; i < 3 * n; i += blockDim.x) hist_rec[2 + i] = ps[i / n][i % n];
+    for (int q = 0; q < 3; ++q)
+      for (int i = threadIdx.x; i < n; i += blockDim.x) hist_rec[2 + q * n + i] = ps[q][i];
   }
 }
