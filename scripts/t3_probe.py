@@ -15,6 +15,11 @@ import time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 
+if os.environ.get("PSG_LIB"):   # A/B a library variant (scripts/ab.py build)
+    from paper_0904_0939_b200 import _lib as _l
+
+    _l.LIB_PATH = os.environ["PSG_LIB"]
+
 from paper_0904_0939_b200 import workloads
 from paper_0904_0939_b200.device import Slab
 
