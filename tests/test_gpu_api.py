@@ -630,14 +630,16 @@ def test_convergence_with_sparse_normalisation(gpu_lib):
         assert d <= 1e-12 * np.max(np.abs(ref.psi.values))
 
 
-@pytest.mark.parametrize("n", [8, 33, 64, 130])
-def test_linear_norm_pairs_match_per_step(gpu_lib, n):
+@pytest.mark.parametrize("n,single", [(8, False), (33, False), (64, False), (130, False),
+                                      (40, True), (96, True)])
+def test_linear_norm_pairs_match_per_step(gpu_lib, n, single):
     """psg_run's linear renormalisation pairs (the default of
     evolve_to_convergence): one two-sweep pass per pair with the pending factor
     applied at the store and the output's norm fused in, against the exact
     per-step path (k_sweep with fused NORM every sweep, the reference's
     arithmetic bitwise) -- odd step counts, checks, re-imposition, an odd
-    offset; fields to 1e-13 of their maximum, norms to 1e-14."""
+    offset, single-buffer slabs (chunked passes); fields to 1e-13 of their
+    maximum, sums to 1e-12."""
     from paper_0904_0939_b200.device import Slab
 
     spec = LatticeSpec(N=n, a=0.4, m=1.0, dtau=0.4 * 0.4 / 4.0)
@@ -645,7 +647,8 @@ def test_linear_norm_pairs_match_per_step(gpu_lib, n):
     init = fill_random_gaussian(allocate(spec), 5)
     runs = []
     for lin in (False, True):
-        with Slab(spec) as s:
+        with Slab(spec, single_buffer=single, chunk=7 if single else 0) as s:
+            s.set_option(12, 0)   # not the small-lattice kernel (plain runs only)
             s.set_field(init.values)
             s.load_grid(grid)
             l0 = s.launches()
