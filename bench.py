@@ -1,7 +1,7 @@
 """Benchmark of the imaginary-time FDTD hot path (driver contract).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config C5|C2|C1|C3|C4a|C4b|C4c]
+                    [--config C5|C2|C1|C3|C4|C4a|C4b|C4c]
 
 A step is one sweep of the whole lattice; the metric is lattice-site updates
 per second (GLUPS), whole job, max over ranks.
@@ -16,7 +16,8 @@ renormalisation every 100 sweeps.  The same lattice at every N:
 with N ranks; fewer visible GPUs than N is an error (``--oversubscribe``
 time-slices the ranks on the visible GPUs -- a protocol check on a smaller
 lattice, never a scaling number).  ``--config C2`` is BASELINE configs[1]
-(Coulomb 256^3); the other configs run through the same code.
+(Coulomb 256^3); the other configs run through the same code; ``--config C4``
+runs config 4 as its whole multi-resolution ladder (128^3 -> 256^3 -> 512^3).
 
 Timed region: exactly K sweeps (with the config's measure / normalise steps)
 bracketed by a barrier + synchronize, CUDA events on the slab's stream, max
@@ -674,6 +675,107 @@ def run_single_gpu(args):
     print(json.dumps(line), flush=True)
 
 
+def run_ladder(args):
+    """--config C4: BASELINE config 4 as the job it is -- the Cornell ladder
+    128^3 -> 256^3 -> 512^3, 5000 sweeps per level, norm / measure every 500.
+    value: the device-resident ladder (start and potentials generated in HBM,
+    resample + renormalise slab to slab on the device), CUDA events around the
+    whole ladder, 3 reps.  e2e: the same ladder through the public API from
+    host arrays (evolve_fixed per level, resample between levels)."""
+    import torch
+
+    from paper_0904_0939_b200 import evolve_fixed, resample, workloads
+    from paper_0904_0939_b200.device import Slab
+    from paper_0904_0939_b200.multires import _renormalize_slab, resample_indices
+
+    levels = [workloads.CONFIGS[k] for k in ("C4a", "C4b", "C4c")]
+    sites = sum(w.N ** 3 * w.steps for w in levels)
+    torch.cuda.set_device(0)
+
+    def resident():
+        prev, launches, e_last = None, 0, []
+        stream0 = None
+        try:
+            for w in levels:
+                spec = w.spec
+                cur = Slab(spec)
+                if prev is None:
+                    workloads.fill_slab(cur, w)
+                else:
+                    cur.fill_potential(*workloads.device_potential(w))
+                    i0, frac = resample_indices(prev.spec, spec)
+                    cur.resample_from(prev, i0, frac)
+                    _renormalize_slab(cur, spec)
+                    prev.close()
+                prev = cur
+                l0 = cur.launches()
+                idx, sums, status = cur.run(w.steps, measure_every=w.measure_every,
+                                            norm_every=w.measure_every)
+                if status.any():
+                    raise SystemExit(f"device status {status} in the ladder")
+                launches += cur.launches() - l0
+                e_last.append(float(np.sum(sums[-1][0]) / np.sum(sums[-1][1])))
+            cur.sync()
+        finally:
+            if prev is not None:
+                prev.close()
+        return launches, e_last
+
+    resident()   # warm-up: every kernel of the ladder once
+    times = []
+    with ClockSampler(0) as clk:
+        for r in range(args.reps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            launches, e_last = resident()
+            torch.cuda.synchronize()
+            times.append(time.perf_counter() - t0)
+    clocks = clk.summary()
+    med, sig = stats(times)
+    value = sites / med / 1e9
+    # e2e: host arrays through the public API (host potentials are setup, outside)
+    grids = [workloads.make_grid(w, w.spec) for w in levels]
+    init = workloads.uniform_field(levels[0].spec)
+    e2e_times, ph = [], []
+    for rep in range(2):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        state = None
+        for w, g in zip(levels, grids):
+            start = init if state is None else resample(state.psi, w.spec)
+            state = evolve_fixed(start, g, w.steps, w.measure_every, norm_every=w.measure_every)
+        e2e_times.append(time.perf_counter() - t0)
+    t_e2e = min(e2e_times)
+    h2d = sum(2 * (w.N + 2) ** 3 * 8 for w in levels)
+    d2h = sum((w.N + 2) ** 3 * 8 for w in levels)
+    steps = sum(w.steps for w in levels)
+    wl = workloads.CONFIGS["C4c"]
+    cfg = bench_config(wl, 1, extra={"workload": "C4_cornell_ladder_128_256_512",
+                                     "N": [w.N for w in levels],
+                                     "a": [w.spec.a for w in levels],
+                                     "dtau": [w.spec.dtau for w in levels],
+                                     "job_steps": steps})
+    line = {
+        "metric": METRIC, "value": value, "unit": "GLUPS", "n_gpus": 1, "steps": steps,
+        "warmup": steps, "ms_per_step": med * 1e3 / steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": cfg,
+        "reps": [round(sites / t / 1e9, 2) for t in times], "sigma_rel": sig,
+        "statistic": f"median of {args.reps} whole ladders (a whole ladder is the step "
+                     "unit: resample + renormalise between levels inside)",
+        "clocks": clocks,
+        "e2e": {"value": sites / t_e2e / 1e9, "unit": "GLUPS", "steps": steps,
+                "h2d_bytes_per_step": h2d / steps, "d2h_bytes_per_step": d2h / steps,
+                "seconds": t_e2e,
+                "api": "evolve_fixed per level from host arrays, resample (GPU) between "
+                       "levels, final psi downloaded; best of 2"},
+        "gpu_launches": launches,
+        "observables": {"E_last_per_level": e_last},
+        "cpu_baseline": None,
+    }
+    print(json.dumps(line), flush=True)
+
+
 def t2_schedule(steps: int, offset: int, m: int):
     """(two-sweep passes, single sweeps) psg_run issues for a fixed run with
     measure / norm every m (the pairing rule of run_loop in csrc/psigpu.cu:
@@ -921,6 +1023,8 @@ def main(argv=None):
         return self_launch(args, argv)
     if world > 1:
         return run_dist(args)
+    if args.config == "C4":
+        return run_ladder(args)
     return run_single_gpu(args)
 
 
