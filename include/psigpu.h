@@ -347,6 +347,13 @@ typedef struct psg_run_params {
  * (whole-lattice slabs; ignored by the multi-slab drivers). */
 #define PSG_RUN_LINEAR_NORM 1
 
+/* psg_run flag: exact.  Every norm / measure step through the per-step path
+ * (plane sums over the sweep's tiles: bitwise the same run on any number of
+ * slabs).  Without it, a small whole lattice (N <= 64, N % 16 == 0, no
+ * re-imposition) runs its norm / measure steps inside the persistent brick
+ * kernel (option 15), within roundoff (1e-13 max|psi|) of the per-step path. */
+#define PSG_RUN_EXACT 2
+
 /* Fused fixed-step driver: runs the evolve_to_convergence loop body
  * (evolve.py:249-270) for `steps` sweeps without host round trips.
  * Measurement records go to hist (host, may be NULL): per check c,
@@ -420,7 +427,10 @@ int psg_tune(psg_slab* s, int blocks_per_sm, int zchunk, int stages);
  * sweeps of a whole lattice with N <= 64, N % 16 == 0 (default 1; bitwise
  * unchanged), 14 = three sweeps per HBM pass (k_sweep3) for runs of plain
  * sweeps of a whole lattice (default 0: measured slower than the two-sweep
- * pass; bitwise unchanged). */
+ * pass; bitwise unchanged), 15 = the persistent brick kernel
+ * also runs the norm / measure steps of a run inside the launch (whole run
+ * without re-imposition in one launch; plane sums over bricks instead of
+ * tiles: within roundoff of the per-step path, not bitwise; default 1). */
 int psg_set_option(psg_slab* s, int option, int value);
 
 /* Enable / disable two sweeps per HBM pass (temporal blocking) for pairs of

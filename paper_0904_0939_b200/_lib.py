@@ -23,6 +23,7 @@ LIB_PATH = os.environ.get("PSG_LIB") or os.path.join(os.path.dirname(os.path.abs
 
 F_WRITE = 1
 RUN_LINEAR_NORM = 1   # psg_run_params.flags: linear renormalisation pairs
+RUN_EXACT = 2         # psg_run_params.flags: norm / measure steps through the per-step path
 F_NORM = 2
 F_MEASURE = 4
 F_CHECK = 8

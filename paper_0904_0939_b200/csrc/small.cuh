@@ -37,6 +37,20 @@ struct SmallArgs {
   int n, pitch, steps;
   int nbi, nbj, nbk;       // bricks per axis
   double h, c0;
+  // in-kernel checks (k_small2<_, true>): the run's norm / measure steps inside
+  // the launch.  State g (global sweep count) is normalised when
+  // norm_every > 0 && g % norm_every == 0 and measured (observables of the
+  // state entering sweep g + 1) when g > 0 && g % measure_every == 0, at most
+  // max_meas times -- run_loop's schedule (evolve.py:249-270).
+  long long g0;            // global index of the state entering the launch
+  long long norm_every, measure_every;
+  int max_meas;
+  const double* fac0;      // factor pending on the input field (&scal[S_ONE] or &scal[S_FACTOR])
+  unsigned long long* nparts;  // [2 parities][bricks][SB_I][2 words]: tagged NORM brick partials
+  double* mparts;          // [max_meas][3][n][nbj * nbk]: observables' brick partials
+  double* scal;
+  const int* bad;
+  double a3, kin, a, center;
 };
 
 // A face value travels as two 64-bit words {32 bits of the double, 32-bit
@@ -161,8 +175,170 @@ constexpr int S2_E = SB_I + 4, S2_J = SB_J + 4, S2_K = SB_K + 4;   // S0 box (ha
 constexpr int SA_E = SB_I + 2, SA_J = SB_J + 2, SA_K = SB_K + 2;   // sweep-A box (halo 1)
 constexpr int SB2_RING = 2 * SB_J * SB_K + 4 * SB_I * SB_K;       // face-ring sites
 constexpr int SB2_SMEM = (S2_E * S2_J * S2_K + SA_E * SA_J * SA_K + 2 * SB2_RING) * 8;
+// in-kernel checks: gathered NORM partials of every brick (N <= 64: at most 128
+// bricks), plane sums, per-warp partials of the norm (8 planes) and of the
+// observables (3 quantities x 8 planes), the factor
+constexpr int SB_MAXB = 128;
+constexpr int SB_WARPS = SB_THREADS / 32;
+constexpr int SB2_CHK_DOUBLES =
+    SB_MAXB * SB_I + 64 + SB_WARPS * SB_I + SB_WARPS * 3 * SB_I + 2 + SB_I * SB_J * SB_K;
+constexpr int SB2_SMEM_CHK = SB2_SMEM + SB2_CHK_DOUBLES * 8;
 
-template <bool FASTC>
+
+// ---- in-kernel checks of k_small2<_, true>: out of line (called ~once per
+// hundred sweeps; keeps the sweep loop's registers those of the plain kernel).
+// Both read the brick's current state from S0 (site (i,j,k) of the brick at
+// S0[((i+2)*S2_J + j+2)*S2_K + k+2]).
+struct SmallChk {
+  double* S0;
+  double* NG;   // [bricks][SB_I] gathered NORM partials
+  double* PS;   // [64] plane sums
+  double* NR;   // [warps][SB_I]
+  double* MR;   // [warps][3][SB_I]
+  double* FS;   // [0] the factor
+  double* VB;   // [SB_I][SB_J][SB_K] the brick's V
+};
+
+// observables of the current state (the brick + one-deep halo): the
+// reference's energy_plane_sums / radius2_plane_sums terms per site
+// (kernels.py:52-100); brick partials per plane (xor butterfly per warp, the
+// warps in ascending order) to dst[q][plane][brick in plane]
+__device__ __noinline__ void small_measure(const SmallChk& k, double* dst,
+                                           long long plane_stride, int pitch, int n, int nbjk, int bjk,
+                                           int i0, int j0, int k0, double kin, double a, double center) {
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int tk = t % SB_K, tj = t / SB_K;
+  auto s0 = [&](int i, int j, int kk) { return k.S0[((i + 2) * S2_J + (j + 2)) * S2_K + (kk + 2)]; };
+  const double dy = __dmul_rn(__dsub_rn((double)(j0 + tj), center), a);
+  const double dz = __dmul_rn(__dsub_rn((double)(k0 + tk), center), a);
+  const double dy2 = __dmul_rn(dy, dy), dz2 = __dmul_rn(dz, dz);
+  // the brick's V, staged in shared memory at kernel start ([SB_I][SB_J][SB_K])
+  double val[32];   // [q][i] slots of this lane, 24 used
+#pragma unroll
+  for (int i = 0; i < SB_I; ++i) {
+    const double p = s0(i, tj, tk);
+    double sl = __dadd_rn(s0(i - 1, tj, tk), s0(i + 1, tj, tk));
+    sl = __dadd_rn(sl, s0(i, tj - 1, tk));
+    sl = __dadd_rn(sl, s0(i, tj + 1, tk));
+    sl = __dadd_rn(sl, s0(i, tj, tk - 1));
+    sl = __dadd_rn(sl, s0(i, tj, tk + 1));
+    sl = __dsub_rn(sl, __dmul_rn(6.0, p));
+    const double hp = __dsub_rn(__dmul_rn(k.VB[(i * SB_J + tj) * SB_K + tk], p), __dmul_rn(kin, sl));
+    const double dx = __dmul_rn(__dsub_rn((double)(i0 + i), center), a);
+    const double rr = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), dy2), dz2);
+    const double w = __dmul_rn(p, p);
+    val[0 * SB_I + i] = __dmul_rn(p, hp);
+    val[1 * SB_I + i] = w;
+    val[2 * SB_I + i] = __dmul_rn(w, rr);
+  }
+#pragma unroll
+  for (int e = 3 * SB_I; e < 32; ++e) val[e] = 0.0;
+  // reduce-scatter over the warp (31 shuffles for the 24 sums): at the step
+  // with offset o a lane keeps the half of its slots selected by bit o of its
+  // lane index and adds its partner's copy of that half; lane l ends with the
+  // warp sum of slot l (a fixed order: deterministic)
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int e = 0; e < o; ++e) {
+      const double send = up ? val[e] : val[e + o];
+      const double keep = up ? val[e + o] : val[e];
+      val[e] = __dadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, o));
+    }
+  }
+  if (lane < 3 * SB_I) k.MR[warp * 3 * SB_I + lane] = val[0];   // slot lane = q * SB_I + i
+  __syncthreads();
+  if (t < 3 * SB_I) {
+    double acc = k.MR[t];
+    for (int w2 = 1; w2 < SB_WARPS; ++w2) acc = __dadd_rn(acc, k.MR[w2 * 3 * SB_I + t]);
+    const int q = t / SB_I, i = t % SB_I;
+    dst[((size_t)q * n + (i0 - 1 + i)) * nbjk + bjk] = acc;
+  }
+  __syncthreads();   // MR free again
+}
+
+// the normalisation factor of the current state: NORM brick partials per
+// plane, a tagged all-gather of every brick's partials, plane sums over the
+// bricks ((bj, bk) ascending), numpy's pairwise total, 1/sqrt(n2) with
+// n2 = total * a^3 (SweepBuffers.renormalize, evolve.py:171-181) -- every
+// block forms the same factor from the same values in the same order.  Block
+// 0 writes the combine's scalars (k_norm_total).  Returns the factor.
+__device__ __noinline__ double small_normalise(const SmallChk& k, unsigned long long* np, uint32_t tag,
+                                               int b, int nbs, int n, int nbjk, double a3, double* scal,
+                                               const int* bad) {
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int tk = t % SB_K, tj = t / SB_K;
+#pragma unroll
+  for (int i = 0; i < SB_I; ++i) {
+    const double c = k.S0[((i + 2) * S2_J + (tj + 2)) * S2_K + (tk + 2)];
+    const double q = warp_sum(__dmul_rn(c, c));
+    if (lane == 0) k.NR[warp * SB_I + i] = q;
+  }
+  __syncthreads();
+  if (t < SB_I) {
+    double acc = k.NR[t];
+    for (int w2 = 1; w2 < SB_WARPS; ++w2) acc = __dadd_rn(acc, k.NR[w2 * SB_I + t]);
+    put_tagged(np + 2 * ((size_t)b * SB_I + t), acc, tag);
+  }
+  constexpr int PER = SB_MAXB * SB_I / SB_THREADS;   // values per thread (at most)
+  const int cnt = nbs * SB_I;
+  unsigned pend = 0;
+#pragma unroll
+  for (int r = 0; r < PER; ++r)
+    if (t + r * SB_THREADS < cnt) pend |= 1u << r;
+  unsigned spins = 0;
+  while (pend) {
+    unsigned long long w0[PER], w1[PER];
+#pragma unroll
+    for (int r = 0; r < PER; ++r)
+      if (pend & (1u << r))
+        asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];"
+                     : "=l"(w0[r]), "=l"(w1[r]) : "l"(np + 2 * (size_t)(t + r * SB_THREADS)) : "memory");
+#pragma unroll
+    for (int r = 0; r < PER; ++r)
+      if ((pend & (1u << r)) && (uint32_t)w0[r] == tag && (uint32_t)w1[r] == tag) {
+        k.NG[t + r * SB_THREADS] =
+            __longlong_as_double((long long)((w1[r] & 0xffffffff00000000ull) | (w0[r] >> 32)));
+        pend &= ~(1u << r);
+      }
+    if (++spins > (1u << 30)) __trap();
+  }
+  __syncthreads();
+  if (t < n) {   // plane t (0-based): brick row t / SB_I, local plane t % SB_I
+    const double* src = k.NG + (size_t)(t / SB_I) * nbjk * SB_I + (t % SB_I);
+    double acc = src[0];
+    for (int q = 1; q < nbjk; ++q) acc = __dadd_rn(acc, src[(size_t)q * SB_I]);
+    k.PS[t] = acc;
+  }
+  __syncthreads();
+  if (t == 0) {
+    const double n2 = __dmul_rn(__dadd_rn(0.0, pw_leaf(k.PS, n)), a3);
+    double f = 1.0;
+    int st = 0;
+    if (n2 == 0.0)
+      st = 3;
+    else if (!finite_d(n2))
+      st = 4;
+    else
+      f = __ddiv_rn(1.0, __dsqrt_rn(n2));
+    k.FS[0] = f;
+    if (b == 0) {   // the combine's scalars (k_norm_total, combine_scalars)
+      scal[S_N2] = n2;
+      scal[S_FACTOR] = f;
+      double status = scal[S_STATUS];
+      if (st && status == 0.0) status = (double)st;
+      if (bad && __ldcg(bad) && status == 0.0) status = 4.0;
+      scal[S_STATUS] = status;
+    }
+  }
+  __syncthreads();
+  const double f = k.FS[0];
+  __syncthreads();   // FS free again
+  return f;
+}
+
+template <bool FASTC, bool CHK>
 __global__ void __launch_bounds__(SB_THREADS, 1) k_small2(const SmallArgs a) {
   extern __shared__ __align__(16) double sm2[];
   double* S0 = sm2;                                   // [S2_E][S2_J][S2_K], site (i,j,k) at (i+2, j+2, k+2)
@@ -186,6 +362,16 @@ __global__ void __launch_bounds__(SB_THREADS, 1) k_small2(const SmallArgs a) {
            ((unsigned)(gk - 1) < (unsigned)n);
   };
   pdl_wait();
+  const double f0 = CHK ? *a.fac0 : 1.0;
+  // check scratch (CHK): after the ring coefficients
+  SmallChk ck;
+  ck.S0 = sm2;
+  ck.NG = sm2 + (S2_E * S2_J * S2_K + SA_E * SA_J * SA_K + 2 * SB2_RING);
+  ck.PS = ck.NG + SB_MAXB * SB_I;
+  ck.NR = ck.PS + 64;
+  ck.MR = ck.NR + SB_WARPS * SB_I;
+  ck.FS = ck.MR + SB_WARPS * 3 * SB_I;
+  ck.VB = ck.FS + 2;
   // S0: the brick with a two-deep halo box from the input field (outside the
   // lattice: padding zeros, or beyond the allocation's planes: zero)
   for (int q = t; q < S2_E * S2_J * S2_K; q += SB_THREADS) {
@@ -193,7 +379,9 @@ __global__ void __launch_bounds__(SB_THREADS, 1) k_small2(const SmallArgs a) {
     const int jj = r % S2_J, ii = r / S2_J;
     const int gi = i0 - 2 + ii, gj = j0 - 2 + jj, gk = k0 - 2 + kk;
     const bool in_box = (gi >= 0) & (gi <= n + 1) & (gj >= 0) & (gj <= n + 1) & (gk >= 0) & (gk <= n + 1);
-    S0[q] = in_box ? a.in[at(gi, gj, gk)] : 0.0;
+    const double x = in_box ? a.in[at(gi, gj, gk)] : 0.0;
+    // a pending normalisation factor: round(psi * f) is the reference's stored psi *= f
+    S0[q] = CHK ? __dmul_rn(x, f0) : x;
   }
   // face-ring site q of this thread's four (two i-face sites, one j-face, one k-face)
   // -> local coordinates; ring index layout: i-lo 0..255, i-hi 256.., j-lo 512, j-hi 640,
@@ -216,7 +404,11 @@ __global__ void __launch_bounds__(SB_THREADS, 1) k_small2(const SmallArgs a) {
   }
   double A[SB_I], C[SB_I], c[SB_I];
 #pragma unroll
-  for (int i = 0; i < SB_I; ++i) coef1<FASTC>(a.v[at(i0 + i, j0 + tj, k0 + tk)], a.h, a.c0, A[i], C[i]);
+  for (int i = 0; i < SB_I; ++i) {
+    const double vi = a.v[at(i0 + i, j0 + tj, k0 + tk)];
+    coef1<FASTC>(vi, a.h, a.c0, A[i], C[i]);
+    if (CHK) ck.VB[(i * SB_J + tj) * SB_K + tk] = vi;
+  }
   __syncthreads();
 #pragma unroll
   for (int i = 0; i < SB_I; ++i) c[i] = s0(i, tj, tk);
@@ -234,9 +426,44 @@ __global__ void __launch_bounds__(SB_THREADS, 1) k_small2(const SmallArgs a) {
   constexpr int F_ILO = 0, F_IHI = 2 * SB_J * SB_K, F_JLO = 4 * SB_J * SB_K;
   constexpr int F_JHI = F_JLO + 2 * SB_I * SB_K, F_KLO = F_JHI + 2 * SB_I * SB_K;
   constexpr int F_KHI = F_KLO + 2 * SB_I * SB_J;
-  int s = 0;
+  // this thread's j- / k-face slots (record offsets of its site i = 0; -1: none)
+  const int joff = tj < 2 ? F_JLO + tj * SB_I * SB_K + tk
+                          : (tj >= SB_J - 2 ? F_JHI + (tj - (SB_J - 2)) * SB_I * SB_K + tk : -1);
+  const int koff = tk < 2 ? F_KLO + tk * SB_I * SB_J + tj
+                          : (tk >= SB_K - 2 ? F_KHI + (tk - (SB_K - 2)) * SB_I * SB_J + tj : -1);
+  // countdowns instead of per-pair 64-bit modulos: dn sweeps to the next
+  // normalised state, dm sweeps to the next measured one (0: the current)
+  // (32-bit: a launch runs at most 2^30 sweeps, so a countdown clamped to
+  // 2^30 + 2 never reaches 0 or 1 when the event lies beyond the launch)
+  constexpr long long CLAMP = (1ll << 30) + 2;
+  int dn = -1, dm = -1, me = 0, nev = 0;
+  if constexpr (CHK) {
+    if (a.norm_every > 0) {
+      dn = (int)min(a.norm_every - a.g0 % a.norm_every, CLAMP);
+      nev = (int)min(a.norm_every, CLAMP);
+    }
+    if (a.measure_every > 0) {
+      const long long lo = a.g0 > 0 ? a.g0 : 1;
+      dm = (int)min((lo + a.measure_every - 1) / a.measure_every * a.measure_every - a.g0, CLAMP);
+      me = (int)min(a.measure_every, CLAMP);
+    }
+  }
+  int s = 0, ex = 0, ne = 0, nm = 0;
   while (s < a.steps) {
-    if (a.steps - s >= 2) {
+    bool pair = a.steps - s >= 2;
+    if constexpr (CHK) {
+      if (dm == 0) {
+        if (nm < a.max_meas) {
+          small_measure(ck, a.mparts + (size_t)nm * 3 * n * (a.nbj * a.nbk), a.plane_stride, a.pitch, n,
+                        a.nbj * a.nbk, bj * a.nbk + bk, i0, j0, k0, a.kin, a.a, a.center);
+          ++nm;
+        }
+        dm = me;
+      }
+      // the state after one sweep is normalised or measured: a single sweep
+      if (dn == 1 || (dm == 1 && nm < a.max_meas)) pair = false;
+    }
+    if (pair) {
       // ---- sweep A: brick (registers) and face ring ----
       double av[SB_I];
 #pragma unroll
@@ -279,24 +506,46 @@ __global__ void __launch_bounds__(SB_THREADS, 1) k_small2(const SmallArgs a) {
       for (int i = 0; i < SB_I; ++i) c[i] = nv[i];
       s += 1;
     }
+    const uint32_t tag = (uint32_t)(a.base + (unsigned long long)s);
+    if constexpr (CHK) {
+      const int k = pair ? 2 : 1;
+      dm -= k;
+      dn -= k;
+      if (dn == 0) {
+        __syncthreads();   // every read of S0 / SA for this sweep is done
+#pragma unroll
+        for (int i = 0; i < SB_I; ++i) s0(i, tj, tk) = c[i];
+        const double f = small_normalise(ck, a.nparts + (size_t)(ne & 1) * nbs * (2 * SB_I), tag, b, nbs, n,
+                                         a.nbj * a.nbk, a.a3, a.scal, a.bad);
+        ++ne;
+#pragma unroll
+        for (int i = 0; i < SB_I; ++i) c[i] = __dmul_rn(c[i], f);
+        dn = nev;
+      }
+    }
     if (s >= a.steps) break;
     __syncthreads();   // every read of S0 / SA for this pair is done
 #pragma unroll
     for (int i = 0; i < SB_I; ++i) s0(i, tj, tk) = c[i];
-    // ---- publish the two-layer faces of the new state (parity by pair) ----
-    const uint32_t tag = (uint32_t)(a.base + (unsigned long long)s);
-    const int par = (s >> 1) & 1;
+    // ---- publish the two-layer faces of the new state (parity by exchange:
+    // a block rewrites a parity only after every neighbour published the
+    // exchange in between, which it did after reading this one) ----
+    const int par = ex & 1;
+    ++ex;
     unsigned long long* f = a.faces + ((size_t)par * nbs + b) * (2 * SB2_FACE);
     put_tagged(f + 2 * (F_ILO + (0 * SB_J + tj) * SB_K + tk), c[0], tag);
     put_tagged(f + 2 * (F_ILO + (1 * SB_J + tj) * SB_K + tk), c[1], tag);
     put_tagged(f + 2 * (F_IHI + (0 * SB_J + tj) * SB_K + tk), c[SB_I - 2], tag);
     put_tagged(f + 2 * (F_IHI + (1 * SB_J + tj) * SB_K + tk), c[SB_I - 1], tag);
+    // j / k faces: one branch per face kind (not one per site: the per-site
+    // divergent branches were a fifth of the kernel's stall samples)
+    if (joff >= 0) {
 #pragma unroll
-    for (int i = 0; i < SB_I; ++i) {
-      if (tj < 2) put_tagged(f + 2 * (F_JLO + (tj * SB_I + i) * SB_K + tk), c[i], tag);
-      if (tj >= SB_J - 2) put_tagged(f + 2 * (F_JHI + ((tj - (SB_J - 2)) * SB_I + i) * SB_K + tk), c[i], tag);
-      if (tk < 2) put_tagged(f + 2 * (F_KLO + (tk * SB_I + i) * SB_J + tj), c[i], tag);
-      if (tk >= SB_K - 2) put_tagged(f + 2 * (F_KHI + ((tk - (SB_K - 2)) * SB_I + i) * SB_J + tj), c[i], tag);
+      for (int i = 0; i < SB_I; ++i) put_tagged(f + 2 * (joff + i * SB_K), c[i], tag);
+    }
+    if (koff >= 0) {
+#pragma unroll
+      for (int i = 0; i < SB_I; ++i) put_tagged(f + 2 * (koff + i * SB_J), c[i], tag);
     }
     // ---- read the halo: faces two deep, the 12 edge lines one deep ----
     // every load of this thread is issued before any tag is checked (one L2
@@ -397,4 +646,35 @@ __global__ void __launch_bounds__(SB_THREADS, 1) k_small2(const SmallArgs a) {
   pdl_launch_dependents();
 #pragma unroll
   for (int i = 0; i < SB_I; ++i) a.out[at(i0 + i, j0 + tj, k0 + tk)] = c[i];
+}
+
+// The checks of a k_small2<_, true> launch: per record, plane sums over the
+// bricks ((bj, bk) ascending) of each observable, numpy's pairwise totals,
+// the scalars and the history record exactly as k_reduce_small forms them
+// (combine_scalars, in record order); the last record's plane sums also to
+// plane_sums.  One block; warp w forms records w, w + 32, ...
+constexpr int SMQ_WARPS = 32;
+constexpr int SMALL_MEAS_MAX = 256;   // records per launch (do_small_chk's cap)
+__global__ void __launch_bounds__(32 * SMQ_WARPS)
+    k_small_meas(const double* __restrict__ mparts, int count, int n, int nbjk, double a3, double* scal,
+                 double* hist, long long rec, double* plane_sums, const int* bad) {
+  __shared__ double tot[SMALL_MEAS_MAX][NQ];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int m = warp; m < count; m += SMQ_WARPS) {
+    double* hr = hist + (size_t)m * rec;
+    for (int e = lane; e < 3 * n; e += 32) {
+      const double* src = mparts + ((size_t)m * 3 * n + e) * nbjk;
+      double acc = src[0];
+      for (int q = 1; q < nbjk; ++q) acc = __dadd_rn(acc, src[q]);
+      hr[2 + e] = acc;
+    }
+    __syncwarp();
+    if (lane < 3) tot[m][lane] = __dadd_rn(0.0, pw_leaf(hr + 2 + lane * n, n));
+    if (lane == 3) tot[m][3] = 0.0;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int m = 0; m < count; ++m) combine_scalars(tot[m], 7u, a3, scal, hist + (size_t)m * rec, bad);
+  if (count > 0)
+    for (int e = threadIdx.x; e < 3 * n; e += blockDim.x) plane_sums[e] = hist[(size_t)(count - 1) * rec + 2 + e];
 }

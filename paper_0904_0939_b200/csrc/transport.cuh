@@ -492,7 +492,33 @@ int run_loop(std::vector<psg_slab*>& sl, Transport* tr, const psg_run_params* p,
     const int64_t sidx = p->step_offset + t;
     return p->reimpose_every > 0 && p->n_impose > 0 && sidx % p->reimpose_every == 0;
   };
-  for (int64_t t = 1; t <= p->steps; ++t) {
+  // a small whole lattice without re-imposition: the whole run, its norm and
+  // measure steps included, in persistent k_small launches (do_small_chk)
+  bool done_small = false;
+  if (whole && s0->small_chk && !(p->flags & PSG_RUN_EXACT) && !(p->reimpose_every > 0 && p->n_impose > 0) &&
+      p->steps >= SMALL_MIN_RUN && small_ok(s0)) {
+    int64_t t = 1;
+    while (t <= p->steps) {
+      const int64_t g0 = p->step_offset + t - 1;
+      int64_t len = std::min<int64_t>(p->steps - t + 1, int64_t(1) << 30);
+      const int64_t room = want - nc;
+      const int64_t me = p->measure_every;
+      if (me > 0 && room > SMALL_MEAS_CAP && small_meas_count(g0, len, me) > SMALL_MEAS_CAP)
+        len = small_first_meas(g0, me) + (int64_t)SMALL_MEAS_CAP * me - g0;   // stop before the next one
+      int nm = 0;
+      {
+        NvtxRange nv("psg:small_run_checks");
+        rc = do_small_chk(s0, len, g0, p->norm_every, me,
+                          (int)std::min<int64_t>(room, SMALL_MEAS_CAP), s0->hist_dev + nc * rec, &nm);
+      }
+      if (rc) return rc;
+      for (int k = 0; k < nm; ++k) steps_of.push_back((double)(small_first_meas(g0, me) + k * me));
+      nc += nm;
+      t += len;
+    }
+    done_small = true;
+  }
+  for (int64_t t = done_small ? p->steps + 1 : 1; t <= p->steps; ++t) {
     if (lin && t + 1 <= p->steps && p->norm_every > 0 &&
         (p->step_offset + t + 1) % p->norm_every == 0 && !meas_at(t) && !reimp_at(t) &&
         !meas_at(t + 1)) {

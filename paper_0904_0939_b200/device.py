@@ -13,7 +13,7 @@ import ctypes
 import numpy as np
 
 from . import _lib
-from ._lib import (F_CHECK, F_MEASURE, F_NORM, F_WRITE, NSCAL, RUN_LINEAR_NORM, RunParams, check,
+from ._lib import (F_CHECK, F_MEASURE, F_NORM, F_WRITE, NSCAL, RUN_EXACT, RUN_LINEAR_NORM, RunParams, check,
                    dptr, lptr)
 from .errors import ConfigError, DeviceError, SingularCoefficientError
 from .lattice import LatticeSpec
@@ -423,14 +423,15 @@ class Slab:
         check(self._lib.psg_resample(coarse._h, self._h, lptr(i0), dptr(frac)))
 
     def _run_params(self, steps, measure_every, norm_every, reimpose_every, constraints,
-                    step_offset, max_checks, linear_norm=False):
+                    step_offset, max_checks, linear_norm=False, exact=False):
         constraints = list(constraints)
         if len(constraints) > 3:
             raise ConfigError("at most 3 parity constraints")
         axes = (ctypes.c_int32 * 3)(*([c[0] for c in constraints] + [0] * (3 - len(constraints))))
         signs = (ctypes.c_int32 * 3)(*([int(c[1]) for c in constraints] + [1] * (3 - len(constraints))))
         p = RunParams(steps, measure_every, norm_every, reimpose_every, step_offset,
-                      len(constraints), axes, signs, RUN_LINEAR_NORM if linear_norm else 0)
+                      len(constraints), axes, signs,
+                      (RUN_LINEAR_NORM if linear_norm else 0) | (RUN_EXACT if exact else 0))
         if max_checks is None:
             max_checks = steps // measure_every + 1 if measure_every > 0 else 0
         hist = np.zeros((max(max_checks, 1), 3 * self.n + 2))
@@ -443,16 +444,21 @@ class Slab:
 
     def run(self, steps: int, measure_every: int = 0, norm_every: int = 1,
             reimpose_every: int = 0, constraints=(), step_offset: int = 0,
-            max_checks: int | None = None, linear_norm: bool = False):
+            max_checks: int | None = None, linear_norm: bool = False, exact: bool = False):
         """Fused fixed-step driver (psg_run).
 
         constraints: sequence of (storage axis, sign) applied in order every
         reimpose_every sweeps.  linear_norm: pairs of sweeps ending on a
         renormalisation run as one renormalising two-sweep pass
-        (PSG_RUN_LINEAR_NORM; within roundoff of the per-step path).  Returns
+        (PSG_RUN_LINEAR_NORM; within roundoff of the per-step path).  exact:
+        every norm / measure step through the per-step path (PSG_RUN_EXACT:
+        tile-ordered plane sums, bitwise the multi-slab engines); otherwise a
+        small whole lattice runs them inside the persistent brick kernel,
+        within roundoff.  Returns
         (state indices, plane sums [c, 3, N] as num|den|r2, per-check status)."""
         p, max_checks, hist = self._run_params(steps, measure_every, norm_every, reimpose_every,
-                                               constraints, step_offset, max_checks, linear_norm)
+                                               constraints, step_offset, max_checks, linear_norm,
+                                               exact)
         nc = ctypes.c_int64()
         check(self._lib.psg_run(self._h, ctypes.byref(p), dptr(hist), max_checks, ctypes.byref(nc)))
         return self._unpack_hist(hist, nc.value)
@@ -512,10 +518,11 @@ def run_multi(slabs, steps: int, measure_every: int = 0, norm_every: int = 1,
               reimpose_every: int = 0, constraints=(), step_offset: int = 0,
               max_checks: int | None = None):
     """psg_run over slabs tiling one lattice, driven by this process (peer
-    copies for the halos; slabs may live on different GPUs)."""
+    copies for the halos; slabs may live on different GPUs).  Always exact
+    (PSG_RUN_EXACT): one slab gives the bits of M slabs."""
     s0 = slabs[0]
     p, max_checks, hist = s0._run_params(steps, measure_every, norm_every, reimpose_every,
-                                         constraints, step_offset, max_checks)
+                                         constraints, step_offset, max_checks, exact=True)
     arr = (ctypes.c_void_p * len(slabs))(*[sl._h for sl in slabs])
     nc = ctypes.c_int64()
     check(s0._lib.psg_run_multi(arr, len(slabs), ctypes.byref(p), dptr(hist), max_checks,

@@ -317,7 +317,9 @@ def evolve_to_convergence(initial: Field3D, grid: PotentialGrid, tol: float = 1e
     the norm of its output fused in; the normalisation after the pair's
     first sweep is subsumed by linearity) -- within roundoff of the
     reference, 2x fewer HBM passes.  ``exact=True`` runs every sweep with its
-    own renormalisation, bitwise the reference's arithmetic.
+    own renormalisation, bitwise the reference's arithmetic (and small
+    lattices run their norm steps through the per-step path, not inside the
+    persistent brick kernel: bitwise evolve_parallel on any number of slabs).
     """
     from .device import Slab
 
@@ -340,7 +342,8 @@ def evolve_to_convergence(initial: Field3D, grid: PotentialGrid, tol: float = 1e
         step_count, converged, checks, snapshots = converge_on_slab(
             slab, grid, tol=tol, check_freq=check_freq, snap_freq=snap_freq,
             constraints=constraints, max_steps=max_steps, max_snapshots=max_snapshots,
-            reimpose_freq=reimpose_freq, norm_every=norm_every, linear_norm=not exact)
+            reimpose_freq=reimpose_freq, norm_every=norm_every, linear_norm=not exact,
+            exact=exact)
         return EvolutionState(psi=Field3D(spec, slab.get_field()), tau=step_count * spec.dtau,
                               step_count=step_count, snapshots=snapshots, checks=checks,
                               converged=converged, constraints=constraints,
@@ -351,7 +354,7 @@ def evolve_to_convergence(initial: Field3D, grid: PotentialGrid, tol: float = 1e
 
 def converge_on_slab(slab, grid: PotentialGrid, *, tol: float, check_freq: int, snap_freq: int,
                      constraints=(), max_steps: int, max_snapshots: int, reimpose_freq: int,
-                     norm_every: int = 1, linear_norm: bool = True):
+                     norm_every: int = 1, linear_norm: bool = True, exact: bool = False):
     """The evolve_to_convergence loop on a device-resident whole-lattice slab
     (its field and potential already in place); leaves the final state on the
     slab.  Returns (step_count, converged, checks, snapshots)."""
@@ -381,7 +384,7 @@ def converge_on_slab(slab, grid: PotentialGrid, *, tol: float, check_freq: int, 
             nxt = min(nxt, (s // snap_freq + 1) * snap_freq)
         slab.run(nxt - s, measure_every=0, norm_every=norm_every,
                  reimpose_every=reimpose_freq if pairs else 0, constraints=pairs,
-                 step_offset=s, linear_norm=linear_norm)
+                 step_offset=s, linear_norm=linear_norm, exact=exact)
         _raise_status(slab.status(), f"before step {nxt}")
         s = nxt
         if s % snap_freq == 0 and len(snapshots) < max_snapshots:
@@ -392,7 +395,7 @@ def converge_on_slab(slab, grid: PotentialGrid, *, tol: float, check_freq: int, 
 def evolve_fixed(initial: Field3D, grid: PotentialGrid, steps: int, measure_every: int,
                  norm_every: int = 1, constraints=(), reimpose_every: int | None = None,
                  slab=None, out: np.ndarray | None = None,
-                 timings: dict | None = None) -> EvolutionState:
+                 timings: dict | None = None, exact: bool = False) -> EvolutionState:
     """Fixed-step run with the observables fused into the sweeps (BASELINE
     configurations: no convergence decisions, so no host round trip until the
     end).  Checks follow evolve_to_convergence's schedule (state indices
@@ -404,7 +407,10 @@ def evolve_fixed(initial: Field3D, grid: PotentialGrid, steps: int, measure_ever
     is downloaded into (it may be ``initial.values`` itself: the start is on
     the device before the run) -- a 2048^3 run then needs two host fields
     (psi, V), not three.  ``timings`` (extension): filled with the
-    perf_counter seconds of the phases (upload, run, download)."""
+    perf_counter seconds of the phases (upload, run, download).  ``exact``
+    (extension): norm / measure steps through the per-step path (bitwise
+    evolve_parallel on any number of slabs); otherwise a small lattice (N <=
+    64) runs them inside its persistent brick kernel, within roundoff."""
     import time
 
     from .device import Slab
@@ -425,7 +431,7 @@ def evolve_fixed(initial: Field3D, grid: PotentialGrid, steps: int, measure_ever
         t1 = time.perf_counter()
         idx, sums, status = slab.run(steps, measure_every=measure_every, norm_every=norm_every,
                                      reimpose_every=reimpose_every if pairs else 0,
-                                     constraints=pairs)
+                                     constraints=pairs, exact=exact)
         _raise_status(slab.status(), "during the run")
         t2 = time.perf_counter()
         checks = []

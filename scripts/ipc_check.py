@@ -55,7 +55,8 @@ def main():
         whole.set_temporal(True)
         whole.set_field(psi0)
         whole.set_potential(v)
-        idx_w, sums_w, _ = whole.run(a.steps, measure_every=every, norm_every=every or 1)
+        idx_w, sums_w, _ = whole.run(a.steps, measure_every=every, norm_every=every or 1,
+                                          exact=True)
         want = whole.get_field()
         from paper_0904_0939_b200.device import measure_multi
 

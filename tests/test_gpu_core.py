@@ -108,6 +108,7 @@ def test_small_lattice_persistent_sweeps_bitwise(gpu_lib, n):
     for small in (0, 1):
         with Slab(spec) as s:
             s.set_option(12, small)
+            s.set_option(15, 0)   # norm / measure steps through the per-step path
             s.set_field(psi)
             s.set_potential(v)
             l0 = s.launches()
@@ -130,6 +131,69 @@ def test_small_lattice_persistent_sweeps_bitwise(gpu_lib, n):
         s.run(9, 0, 0)
         assert s.launches() - l0 == 1
         assert np.array_equal(s.get_field(), want)
+
+
+@pytest.mark.parametrize("n,steps,me,ne,off", [
+    (16, 57, 20, 20, 1), (32, 61, 7, 5, 0), (48, 40, 10, 1, 3), (64, 300, 100, 100, 0),
+    (64, 41, 0, 2, 0), (32, 600, 1, 3, 0)])
+def test_small_lattice_checks_in_kernel(gpu_lib, n, steps, me, ne, off):
+    """k_small2 with the run's norm / measure steps inside the launch (option
+    15): the schedule, history records and status of the per-step path; the
+    field within 1e-13 max|psi| and every plane sum within 1e-12 relative (the
+    plane sums run over bricks instead of tiles); fewer launches.  The last
+    case records 600 observables (three launches of at most 256)."""
+    spec, psi, v = _case(n, 900 + n, pad=0.0)
+    outs = []
+    for chk in (0, 1):
+        with Slab(spec) as s:
+            s.set_option(15, chk)
+            s.set_field(psi)
+            s.set_potential(v)
+            l0 = s.launches()
+            idx, sums, st = s.run(steps, measure_every=me, norm_every=ne, step_offset=off)
+            outs.append((s.get_field(), idx, sums, st, s.launches() - l0))
+    (f0, i0, s0, st0, l0), (f1, i1, s1, st1, l1) = outs
+    assert list(i0) == list(i1)
+    assert np.array_equal(st0, st1)
+    assert np.abs(f1 - f0).max() <= 1e-13 * np.abs(f0).max()
+    if len(s0):
+        np.testing.assert_allclose(s1, s0, rtol=1e-12, atol=1e-13 * np.abs(s0).max())
+    assert l1 < l0
+
+
+def test_small_lattice_checks_pending_factor_and_oracle(gpu_lib):
+    """A run ending on a norm step through the per-step path leaves the factor
+    pending; the next run's k_small2 launch folds it into its loads.  The two
+    runs together equal the oracle's fixed-step evolution (BASELINE config 1
+    cadence at 32^3) within 1e-12 max|psi|, energies within 1e-10."""
+    n = 32
+    spec = LatticeSpec(N=n, a=0.15 * 64 / n, m=1.0, dtau=(0.15 * 64 / n) ** 2 / 4.0)
+    rng = np.random.default_rng(77)
+    psi0 = np.zeros((n + 2,) * 3)
+    psi0[1:-1, 1:-1, 1:-1] = rng.uniform(-0.5, 0.5, (n, n, n))
+    c = np.arange(1, n + 1) - (n + 1) / 2.0
+    x = c * spec.a
+    v = np.zeros((n + 2,) * 3)
+    v[1:-1, 1:-1, 1:-1] = 0.5 * (x[:, None, None] ** 2 + x[None, :, None] ** 2 + x[None, None, :] ** 2)
+    want, checks = O.evolve_fixed(psi0, v, n, spec.a, spec.m, spec.dtau, 400, 100, norm_every=100)
+    with Slab(spec) as s:
+        s.set_field(psi0)
+        s.set_potential(v)
+        s.set_option(15, 0)
+        i1, sm1, st1 = s.run(100, measure_every=100, norm_every=100)
+        s.set_option(15, 1)
+        l0 = s.launches()
+        i2, sm2, st2 = s.run(300, measure_every=100, norm_every=100, step_offset=100)
+        assert s.launches() - l0 == 2   # k_small2 + the checks' reduce
+        got = s.get_field()
+    assert not st1.any() and not st2.any()
+    assert list(i1) + list(i2) == [c[0] for c in checks]
+    assert np.abs(got - want).max() <= 1e-12 * np.abs(want).max()
+    for c, sm in zip(checks, list(sm1) + list(sm2)):
+        e = float(np.sum(sm[0])) / float(np.sum(sm[1]))
+        assert abs(e - c[1]) <= 1e-10 * abs(c[1])
+        r = math.sqrt(float(np.sum(sm[2])) / float(np.sum(sm[1])))
+        assert abs(r - c[3]) <= 1e-10 * abs(c[3])
 
 
 def test_new_potential_clears_coefficient_mode(gpu_lib):
