@@ -426,11 +426,7 @@ __global__ void __launch_bounds__(SB_THREADS, 1) k_small2(const SmallArgs a) {
   constexpr int F_ILO = 0, F_IHI = 2 * SB_J * SB_K, F_JLO = 4 * SB_J * SB_K;
   constexpr int F_JHI = F_JLO + 2 * SB_I * SB_K, F_KLO = F_JHI + 2 * SB_I * SB_K;
   constexpr int F_KHI = F_KLO + 2 * SB_I * SB_J;
-  // this thread's j- / k-face slots (record offsets of its site i = 0; -1: none)
-  const int joff = tj < 2 ? F_JLO + tj * SB_I * SB_K + tk
-                          : (tj >= SB_J - 2 ? F_JHI + (tj - (SB_J - 2)) * SB_I * SB_K + tk : -1);
-  const int koff = tk < 2 ? F_KLO + tk * SB_I * SB_J + tj
-                          : (tk >= SB_K - 2 ? F_KHI + (tk - (SB_K - 2)) * SB_I * SB_J + tj : -1);
+  static_assert(SB_J == 16 && SB_K == 16 && SB_I == 8, "face publishing assumes 8 x 16 x 16 bricks");
   // countdowns instead of per-pair 64-bit modulos: dn sweeps to the next
   // normalised state, dm sweeps to the next measured one (0: the current)
   // (32-bit: a launch runs at most 2^30 sweeps, so a countdown clamped to
@@ -537,15 +533,19 @@ __global__ void __launch_bounds__(SB_THREADS, 1) k_small2(const SmallArgs a) {
     put_tagged(f + 2 * (F_ILO + (1 * SB_J + tj) * SB_K + tk), c[1], tag);
     put_tagged(f + 2 * (F_IHI + (0 * SB_J + tj) * SB_K + tk), c[SB_I - 2], tag);
     put_tagged(f + 2 * (F_IHI + (1 * SB_J + tj) * SB_K + tk), c[SB_I - 1], tag);
-    // j / k faces: one branch per face kind (not one per site: the per-site
-    // divergent branches were a fifth of the kernel's stall samples)
-    if (joff >= 0) {
+    // j / k faces (1024 values) from the new brick in S0, four per thread,
+    // each warp storing 32 consecutive record slots: from the owners'
+    // registers they were 8 scattered stores on 4 lanes of every warp (a
+    // store-queue stall) or per-site divergent branches
+    __syncthreads();   // the brick in S0
 #pragma unroll
-      for (int i = 0; i < SB_I; ++i) put_tagged(f + 2 * (joff + i * SB_K), c[i], tag);
-    }
-    if (koff >= 0) {
-#pragma unroll
-      for (int i = 0; i < SB_I; ++i) put_tagged(f + 2 * (koff + i * SB_J), c[i], tag);
+    for (int r = 0; r < 4; ++r) {
+      const int e = t + SB_THREADS * r;           // [kind j|k][side lo|hi][layer][i][x]
+      const int side = (e >> 8) & 1, layer = (e >> 7) & 1, i = (e >> 4) & 7, x = e & 15;
+      const int w = side ? SB_J - 2 + layer : layer;   // SB_J == SB_K
+      const double val = r < 2 ? s0(i, w, x) : s0(i, x, w);
+      const int off = (r < 2 ? (side ? F_JHI : F_JLO) : (side ? F_KHI : F_KLO)) + (layer * SB_I + i) * 16 + x;
+      put_tagged(f + 2 * off, val, tag);
     }
     // ---- read the halo: faces two deep, the 12 edge lines one deep ----
     // every load of this thread is issued before any tag is checked (one L2
