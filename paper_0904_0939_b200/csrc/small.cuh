@@ -45,6 +45,7 @@ struct SmallArgs {
   long long g0;            // global index of the state entering the launch
   long long norm_every, measure_every;
   int max_meas;
+  int linear;              // PSG_RUN_LINEAR_NORM with norm_every == 1: pairs, one normalisation per pair
   const double* fac0;      // factor pending on the input field (&scal[S_ONE] or &scal[S_FACTOR])
   unsigned long long* nparts;  // [2 parities][bricks][SB_I][2 words]: tagged NORM brick partials
   double* mparts;          // [max_meas][3][n][nbj * nbk]: observables' brick partials
@@ -456,8 +457,10 @@ __global__ void __launch_bounds__(SB_THREADS, 1) k_small2(const SmallArgs a) {
         }
         dm = me;
       }
-      // the state after one sweep is normalised or measured: a single sweep
-      if (dn == 1 || (dm == 1 && nm < a.max_meas)) pair = false;
+      // the state after one sweep is normalised or measured: a single sweep --
+      // unless it is a linear pair (every state normalised: the pair's
+      // normalisation subsumes its first sweep's, S(f psi) = f S(psi))
+      if ((dn == 1 && !a.linear) || (dm == 1 && nm < a.max_meas)) pair = false;
     }
     if (pair) {
       // ---- sweep A: brick (registers) and face ring ----
@@ -507,7 +510,7 @@ __global__ void __launch_bounds__(SB_THREADS, 1) k_small2(const SmallArgs a) {
       const int k = pair ? 2 : 1;
       dm -= k;
       dn -= k;
-      if (dn == 0) {
+      if (nev > 0 && dn <= 0) {   // (< 0: a linear pair passed two normalised states)
         __syncthreads();   // every read of S0 / SA for this sweep is done
 #pragma unroll
         for (int i = 0; i < SB_I; ++i) s0(i, tj, tk) = c[i];

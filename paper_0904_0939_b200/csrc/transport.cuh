@@ -508,8 +508,8 @@ int run_loop(std::vector<psg_slab*>& sl, Transport* tr, const psg_run_params* p,
       int nm = 0;
       {
         NvtxRange nv("psg:small_run_checks");
-        rc = do_small_chk(s0, len, g0, p->norm_every, me,
-                          (int)std::min<int64_t>(room, SMALL_MEAS_CAP), s0->hist_dev + nc * rec, &nm);
+        rc = do_small_chk(s0, len, g0, p->norm_every, me, (int)std::min<int64_t>(room, SMALL_MEAS_CAP),
+                          (p->flags & PSG_RUN_LINEAR_NORM) != 0, s0->hist_dev + nc * rec, &nm);
       }
       if (rc) return rc;
       for (int k = 0; k < nm; ++k) steps_of.push_back((double)(small_first_meas(g0, me) + k * me));

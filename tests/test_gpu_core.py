@@ -161,6 +161,33 @@ def test_small_lattice_checks_in_kernel(gpu_lib, n, steps, me, ne, off):
     assert l1 < l0
 
 
+@pytest.mark.parametrize("n,steps,me,off", [(32, 81, 10, 0), (64, 200, 100, 1), (48, 57, 7, 2)])
+def test_small_lattice_linear_pairs_in_kernel(gpu_lib, n, steps, me, off):
+    """evolve_to_convergence's default cadence (renormalise every sweep, linear
+    pairs allowed) inside k_small2: pairs of sweeps with one normalisation per
+    pair, singles where the state between them is measured.  Within 1e-13
+    max|psi| of the exact per-step path, same records within 1e-12; fewer
+    launches than the renormalising two-sweep passes."""
+    spec, psi, v = _case(n, 1300 + n, pad=0.0)
+    outs = []
+    for chk, lin, exact in ((0, False, True), (0, True, False), (1, True, False)):
+        with Slab(spec) as s:
+            s.set_option(15, chk)
+            s.set_field(psi)
+            s.set_potential(v)
+            l0 = s.launches()
+            idx, sums, st = s.run(steps, measure_every=me, norm_every=1, step_offset=off,
+                                  linear_norm=lin, exact=exact)
+            outs.append((s.get_field(), list(idx), np.asarray(sums), st, s.launches() - l0))
+    ref = outs[0]
+    for got in outs[1:]:
+        assert got[1] == ref[1]
+        assert not got[3].any()
+        assert np.abs(got[0] - ref[0]).max() <= 1e-13 * np.abs(ref[0]).max()
+        np.testing.assert_allclose(got[2], ref[2], rtol=1e-12, atol=1e-13 * np.abs(ref[2]).max())
+    assert outs[2][4] < outs[1][4]
+
+
 def test_small_lattice_checks_pending_factor_and_oracle(gpu_lib):
     """A run ending on a norm step through the per-step path leaves the factor
     pending; the next run's k_small2 launch folds it into its loads.  The two
