@@ -298,7 +298,8 @@ template <int S, int TB, bool STEP2, bool FASTC, bool MASK, bool PEER = false, b
 __device__ __forceinline__ void t2b_rows_item(const SweepArgs& args, const T2Item& I,
                                               uint32_t fb, uint32_t base, int w, int lane,
                                               StageRot<S, T2BGeo<TB>::STAGE>& nx, uint32_t& g,
-                                              double fnorm = 1.0, double* qacc = nullptr) {
+                                              double fnorm = 1.0, double* qacc = nullptr,
+                                              bool peer_edge = false) {
   using G = T2BGeo<TB>;
   using C = T2BCfg<S, TB>;
   constexpr uint32_t VOFF = G::PSI_STRIDE - BOXW * 8;  // V box starts one row lower
@@ -391,17 +392,6 @@ __device__ __forceinline__ void t2b_rows_item(const SweepArgs& args, const T2Ite
         if (!MASK || ok0) *qacc = __fma_rn(o0, o0, *qacc);
         if (!MASK || ok1) *qacc = __fma_rn(o1, o1, *qacc);
       }
-      if (PEER) {
-        const int z = p - 1;   // the output plane (uniform across the block)
-        const long long dd = z <= args.pl_hi ? args.dl : (z >= args.pr_lo ? args.dr : 0);
-        if (dd != 0) {
-          if (!MASK || ok1) {
-            *reinterpret_cast<double2*>(dst + dd) = make_double2(o0, o1);
-          } else if (ok0) {
-            dst[dd] = o0;
-          }
-        }
-      }
     }
     if (STEP2) doff += pstride;
     rg.next(rf0);
@@ -423,6 +413,24 @@ __device__ __forceinline__ void t2b_rows_item(const SweepArgs& args, const T2Ite
   }
   g += (uint32_t)(pend - (I.z0 - 1));
   mbar_arrive_u(cur_bar + S * 8);
+  if (PEER && STEP2 && peer_edge) {
+    // the fused exchange: this item's edge output planes (z <= pl_hi go to the
+    // left neighbour's halo, z >= pr_lo to the right one's) copied after the
+    // plane loop from the lane's own just-stored sites (same thread: program
+    // order) -- inside the loop the peer stores and their 64-bit offsets cost
+    // the loop its registers (312 B of stack at 96 registers, +47 % per pass)
+    const long long base_off = (long long)j * args.pitch + (k + COL_OFF);
+    auto copy_plane = [&](int z, long long dd) {
+      const double* src = args.out + ((long long)(z - args.z_base) * args.plane_stride + base_off);
+      if (!MASK || ok1) {
+        *reinterpret_cast<double2*>(const_cast<double*>(src) + dd) = *reinterpret_cast<const double2*>(src);
+      } else if (ok0) {
+        const_cast<double*>(src)[dd] = src[0];
+      }
+    };
+    for (int z = I.z0; z <= min(I.z1, args.pl_hi); ++z) copy_plane(z, args.dl);
+    for (int z = max(I.z0, args.pr_lo); z <= I.z1; ++z) copy_plane(z, args.dr);
+  }
   if (STEP2 && I.idx < args.sig_items) {
     // an edge item's planes are stored: make them visible, then count this
     // warp done (the exchange waits for the count on its own stream)
@@ -444,13 +452,13 @@ __device__ __forceinline__ void t2b_rows(const SweepArgs& args, uint32_t sm0, in
     t2b_for_items<TB>(args, [&](const T2Item& I) {
       // only items holding an edge output plane take the peer-store variant
       const bool edge = I.z0 <= args.pl_hi || I.z1 >= args.pr_lo;
-      if (t2b_row_interior(I, w, args.n, args.x_off)) {
-        if (edge) t2b_rows_item<S, TB, STEP2, FASTC, false, true>(args, I, fb, base, w, lane, nx, g);
-        else t2b_rows_item<S, TB, STEP2, FASTC, false, false>(args, I, fb, base, w, lane, nx, g);
-      } else {
-        if (edge) t2b_rows_item<S, TB, STEP2, FASTC, true, true>(args, I, fb, base, w, lane, nx, g);
-        else t2b_rows_item<S, TB, STEP2, FASTC, true, false>(args, I, fb, base, w, lane, nx, g);
-      }
+      // (a runtime flag, not two more inlined variants: the larger body was not
+      // inlined, which put the kernel's parameters on the stack -- 312 B,
+      // +47 % per pass at 512^2 x 256, profiles/fused_pass_r02.txt)
+      if (t2b_row_interior(I, w, args.n, args.x_off))
+        t2b_rows_item<S, TB, STEP2, FASTC, false, true>(args, I, fb, base, w, lane, nx, g, 1.0, nullptr, edge);
+      else
+        t2b_rows_item<S, TB, STEP2, FASTC, true, true>(args, I, fb, base, w, lane, nx, g, 1.0, nullptr, edge);
     });
     // no fence here: the peer stores are performed when this grid completes;
     // whoever reads them is ordered after that completion (an event, or the
