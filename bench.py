@@ -946,7 +946,7 @@ def run_dist(args):
                           max_steps=40, max_snapshots=0, norm_every=10, fixed=True)
     selfcheck = None
     if rank == 0:
-        one = evolve_fixed(init, cgrid, 40, 10, norm_every=10)
+        one = evolve_fixed(init, cgrid, 40, 10, norm_every=10, exact=True)   # the per-step path
         selfcheck = {"N": n_chk, "steps": 40, "slabs": world,
                      "psi_bitwise": bool(np.array_equal(stp.psi.values, one.psi.values)),
                      "energies_bitwise": [c.energy for c in stp.checks]

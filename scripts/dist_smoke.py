@@ -65,7 +65,7 @@ def main():
     st = evolve_parallel(grid, workers=world, initial=init, transport="nccl", check_freq=20,
                          max_steps=100, max_snapshots=0, norm_every=20, fixed=True)
     if rank == 0:
-        ref = evolve_fixed(init, grid, 100, 20, norm_every=20)
+        ref = evolve_fixed(init, grid, 100, 20, norm_every=20, exact=True)
         same = np.array_equal(st.psi.values, ref.psi.values)
         e_same = [c.energy for c in st.checks] == [c.energy for c in ref.checks]
         print(f"dist_smoke fixed: psi bitwise {same}, energies bitwise {e_same}", flush=True)
@@ -75,7 +75,7 @@ def main():
                          transport="nccl", scatter_initial=True, check_freq=20, max_steps=60,
                          max_snapshots=0, norm_every=20, fixed=True)
     if rank == 0:
-        ref = evolve_fixed(init, grid, 60, 20, norm_every=20)
+        ref = evolve_fixed(init, grid, 60, 20, norm_every=20, exact=True)
         same = np.array_equal(st.psi.values, ref.psi.values)
         print(f"dist_smoke scatter/gather: psi bitwise {same}", flush=True)
         ok = ok and same
