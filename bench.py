@@ -498,7 +498,7 @@ def time_pass(slab, st, npass, reserve_sms=0):
 
 
 def small_lattice(n) -> bool:
-    """Runs of plain sweeps go through k_small (psigpu.cu small_ok: N <= 64, N % 16 == 0)."""
+    """Whole runs go through k_small2 (psigpu.cu small_ok: N <= 64, N % 16 == 0)."""
     return n <= 64 and n % 16 == 0
 
 
@@ -511,14 +511,18 @@ def roofline(n, pass_s, glups, per_pass_launches, sites_per_gpu=None):
            "frac_basis": "24 B/site of HBM per two-sweep pass (psi read, V read, psi write) / "
                          "pass duration / measured copy bandwidth",
            "frac_per_update_basis": BYTES_PER_SITE * glups / peak,
-           "kernel": ("k_small (persistent brick kernel: a run of plain sweeps in one launch; "
-                      "'pass' = two of its sweeps)" if small_lattice(n) and sites_per_gpu is None
+           "kernel": ("k_small2 (persistent brick kernel: the whole run, norm and measure steps "
+                      "included, in one launch; 'pass' = two of its sweeps)"
+                      if small_lattice(n) and sites_per_gpu is None
                       else "k_sweep2b (two fp64 7-point sweeps per HBM pass, TMA z-march)"
                       + (f", {per_pass_launches} launches per pass" if per_pass_launches > 1
                          else "")),
            "pass_us": pass_s * 1e6, "peak_source": peak_kind,
            "algorithmic_bytes_per_pass": BYTES_PER_SITE * sites,
            "site_updates_per_pass": 2 * sites, "traffic": None}
+    if small_lattice(n) and sites_per_gpu is None:
+        rec["note"] = (f"the {n}^3 lattice ({3 * 8 * (n + 2) ** 3 / 1e6:.1f} MB of fields) stays in the "
+                       "126 MB L2: the run is bound by the bricks' face-exchange latency, not HBM")
     t = load_traffic(n)
     if t and sites == n ** 3:
         rec["traffic"] = t["dram_bytes_per_pass"]

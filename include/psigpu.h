@@ -423,7 +423,7 @@ int psg_tune(psg_slab* s, int blocks_per_sm, int zchunk, int stages);
  * two-sweep pass also stores its edge output planes into the neighbouring
  * slabs' halo planes through peer memory (NVLink between GPUs) instead of a
  * separate copy; needs W >= 4 and peer access, else the copies are used
- * (bitwise unchanged), 12 = persistent brick kernel (k_small) for runs of plain
+ * (bitwise unchanged), 12 = persistent brick kernel (k_small2) for runs of plain
  * sweeps of a whole lattice with N <= 64, N % 16 == 0 (default 1; bitwise
  * unchanged), 14 = three sweeps per HBM pass (k_sweep3) for runs of plain
  * sweeps of a whole lattice (default 0: measured slower than the two-sweep
