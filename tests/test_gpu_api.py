@@ -662,3 +662,22 @@ def test_linear_norm_pairs_match_per_step(gpu_lib, n, single):
     assert np.abs(f1 - f0).max() <= 1e-13 * np.abs(f0).max()
     np.testing.assert_allclose(s1, s0, rtol=1e-12, atol=1e-300)
     assert l1 < l0     # pairs went through the renormalising pass
+
+
+@pytest.mark.parametrize("exact", [False, True])
+def test_small_lattice_error_paths(gpu_lib, exact):
+    """The persistent small-lattice kernel (norm steps inside the launch) keeps
+    the reference's error behaviour: a zero start raises ZeroNormError at the
+    first renormalisation, an unstable dtau DivergenceError within 500 sweeps
+    (evolve.py:171-181, 249-262) -- and so does the exact per-step path."""
+    spec, grid = free_box(16, a=1.0)
+    with pytest.raises(ZeroNormError):
+        evolve_to_convergence(allocate(spec), grid, check_freq=10, max_steps=50, exact=exact)
+    spec = LatticeSpec(N=16, a=1.0, m=1.0, dtau=1.05 / 3.0)
+    grid = custom(spec, np.zeros((16, 16, 16)))
+    with pytest.raises(DivergenceError):
+        evolve_to_convergence(fill_random_gaussian(allocate(spec), 4), grid, tol=1e-6,
+                              check_freq=100, max_steps=500, exact=exact)
+    spec, grid = free_box(32, a=1.0)
+    with pytest.raises(ZeroNormError):
+        evolve_fixed(allocate(spec), grid, 40, 10, norm_every=10, exact=exact)
