@@ -294,7 +294,8 @@ __device__ __forceinline__ bool t2b_ring_interior(const T2Item& I, int n, int x_
 // writes args.part[nslot + block * TB + warp - 1] for k_norm_total.  No
 // per-plane sums: a whole-lattice slab needs only the total (per-plane
 // butterflies cost +31 % instructions, measured).
-template <int S, int TB, bool STEP2, bool FASTC, bool MASK, bool PEER = false, bool NRM = false>
+template <int S, int TB, bool STEP2, bool FASTC, bool MASK, bool PEER = false, bool NRM = false,
+          bool MS = false>
 __device__ __forceinline__ void t2b_rows_item(const SweepArgs& args, const T2Item& I,
                                               uint32_t fb, uint32_t base, int w, int lane,
                                               StageRot<S, T2BGeo<TB>::STAGE>& nx, uint32_t& g,
@@ -360,6 +361,51 @@ __device__ __forceinline__ void t2b_rows_item(const SweepArgs& args, const T2Ite
     } else {
       qw = make_double2(u0, u1);
     }
+    if constexpr (MS && STEP2) {
+      if (p >= I.z0 && p <= I.z1) {   // this item's own planes (block-uniform)
+        // observables of the pass's input state on this lane's two sites: the
+        // reference's energy_plane_sums / radius2_plane_sums terms
+        // (kernels.py:52-100) from step 1's operands; the input carries the
+        // pending factor f, applied by linearity: sums x f^2
+        double s0 = __dadd_rn(cp.x, cn.x);
+        s0 = __dadd_rn(s0, jm.x);
+        s0 = __dadd_rn(s0, jp.x);
+        s0 = __dadd_rn(s0, km);
+        s0 = __dadd_rn(s0, cc.y);
+        s0 = __dsub_rn(s0, __dmul_rn(6.0, cc.x));
+        double s1 = __dadd_rn(cp.y, cn.y);
+        s1 = __dadd_rn(s1, jm.y);
+        s1 = __dadd_rn(s1, jp.y);
+        s1 = __dadd_rn(s1, cc.x);
+        s1 = __dadd_rn(s1, kp);
+        s1 = __dsub_rn(s1, __dmul_rn(6.0, cc.y));
+        const double h0 = __dsub_rn(__dmul_rn(v.x, cc.x), __dmul_rn(args.kin, s0));
+        const double h1 = __dsub_rn(__dmul_rn(v.y, cc.y), __dmul_rn(args.kin, s1));
+        const double dx = __dmul_rn(__dsub_rn((double)(args.x_off + p), args.center), args.a);
+        const double dy = __dmul_rn(__dsub_rn((double)j, args.center), args.a);
+        const double dza = __dmul_rn(__dsub_rn((double)k, args.center), args.a);
+        const double dzb = __dmul_rn(__dsub_rn((double)(k + 1), args.center), args.a);
+        const double dxy = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
+        const double w0 = __dmul_rn(cc.x, cc.x), w1 = __dmul_rn(cc.y, cc.y);
+        double r_num = __dadd_rn(ok0 ? __dmul_rn(cc.x, h0) : 0.0, ok1 ? __dmul_rn(cc.y, h1) : 0.0);
+        double r_den = __dadd_rn(ok0 ? w0 : 0.0, ok1 ? w1 : 0.0);
+        double r_r2 = __dadd_rn(ok0 ? __dmul_rn(w0, __dadd_rn(dxy, __dmul_rn(dza, dza))) : 0.0,
+                                ok1 ? __dmul_rn(w1, __dadd_rn(dxy, __dmul_rn(dzb, dzb))) : 0.0);
+        r_num = warp_sum(r_num);
+        r_den = warp_sum(r_den);
+        r_r2 = warp_sum(r_r2);
+        if (lane == 0) {   // [q][plane][tile row]: one slot per (tile, row) of the plane
+          const long long tx = (long long)args.tiles * TB;
+          const long long slot = (long long)p * tx +
+                                 (long long)((I.j - 1) / TB * args.tiles_k + (I.k - 1) / TX) * TB + (w - 1);
+          const long long qs = (long long)args.planes * tx;
+          const double f2 = __dmul_rn(fnorm, fnorm);
+          args.part[slot] = __dmul_rn(r_num, f2);
+          args.part[qs + slot] = __dmul_rn(r_den, f2);
+          args.part[2 * qs + slot] = __dmul_rn(r_r2, f2);
+        }
+      }
+    }
     sts2_u(base + ROFF + rg.rw, qw);
     mbar_arrive_u(cur_bar + S * 8);
     mbar_arrive_u(rg.bw);
@@ -378,7 +424,7 @@ __device__ __forceinline__ void t2b_rows_item(const SweepArgs& args, const T2Ite
       const double rkp = lds1_u(rq + 16);
       double o0 = upd(am.x, fm.x, qm.x, qmm.x, qw.x, rjm.x, rjp.x, rkm, qm.y);
       double o1 = upd(am.y, fm.y, qm.y, qmm.y, qw.y, rjm.y, rjp.y, qm.x, rkp);
-      if (NRM) {
+      if (NRM || MS) {   // the input's pending factor, applied at the store by linearity
         o0 = __dmul_rn(o0, fnorm);
         o1 = __dmul_rn(o1, fnorm);
       }
@@ -440,7 +486,7 @@ __device__ __forceinline__ void t2b_rows_item(const SweepArgs& args, const T2Ite
   }
 }
 
-template <int S, int TB, bool STEP2, bool FASTC, bool PEER = false, bool NRM = false>
+template <int S, int TB, bool STEP2, bool FASTC, bool PEER = false, bool NRM = false, bool MS = false>
 __device__ __forceinline__ void t2b_rows(const SweepArgs& args, uint32_t sm0, int w, int lane,
                                          double fnorm = 1.0) {
   using C = T2BCfg<S, TB>;
@@ -468,11 +514,11 @@ __device__ __forceinline__ void t2b_rows(const SweepArgs& args, uint32_t sm0, in
     double qacc = 0.0;
     t2b_for_items<TB>(args, [&](const T2Item& I) {
       if (t2b_row_interior(I, w, args.n, args.x_off))
-        t2b_rows_item<S, TB, STEP2, FASTC, false, false, NRM>(args, I, fb, base, w, lane, nx, g, fnorm,
-                                                             &qacc);
+        t2b_rows_item<S, TB, STEP2, FASTC, false, false, NRM, MS>(args, I, fb, base, w, lane, nx, g, fnorm,
+                                                                 &qacc);
       else
-        t2b_rows_item<S, TB, STEP2, FASTC, true, false, NRM>(args, I, fb, base, w, lane, nx, g, fnorm,
-                                                            &qacc);
+        t2b_rows_item<S, TB, STEP2, FASTC, true, false, NRM, MS>(args, I, fb, base, w, lane, nx, g, fnorm,
+                                                                &qacc);
     });
     if constexpr (NRM && STEP2) {
       qacc = warp_sum(qacc);
@@ -568,7 +614,7 @@ __device__ __forceinline__ void t2b_ringw(const SweepArgs& args, uint32_t sm0, i
   });
 }
 
-template <int NST, int TB, bool FASTC, bool PEER = false, bool NRM = false>
+template <int NST, int TB, bool FASTC, bool PEER = false, bool NRM = false, bool MS = false>
 __global__ void __launch_bounds__(T2BGeo<TB>::THREADS, T2BGeo<TB>::MINB)
     k_sweep2b(const __grid_constant__ CUtensorMap tm_psi, const __grid_constant__ CUtensorMap tm_v,
               const SweepArgs args) {
@@ -627,8 +673,9 @@ __global__ void __launch_bounds__(T2BGeo<TB>::THREADS, T2BGeo<TB>::MINB)
     t2b_rows<S, TB, false, FASTC>(args, sm0, warp, lane);
   } else {
     static_assert(!(PEER && NRM), "no fused exchange in the renormalising pass");
-    const double fnorm = NRM ? *args.scale : 1.0;   // after pdl_wait: the predecessor's factor
-    t2b_rows<S, TB, true, FASTC, PEER, NRM>(args, sm0, warp, lane, fnorm);
+    static_assert(!(MS && (PEER || NRM)), "the measuring pass is a plain whole-lattice pass");
+    const double fnorm = (NRM || MS) ? *args.scale : 1.0;   // after pdl_wait: the predecessor's factor
+    t2b_rows<S, TB, true, FASTC, PEER, NRM, MS>(args, sm0, warp, lane, fnorm);
   }
 }
 

@@ -518,7 +518,42 @@ int run_loop(std::vector<psg_slab*>& sl, Transport* tr, const psg_run_params* p,
     }
     done_small = true;
   }
+  // norm / measure steps of a whole lattice inside two-sweep passes (option
+  // 16; PSG_RUN_EXACT opts out): a pair ending on a normalisation runs as a
+  // renormalising pass (the norm of its output, no factor to subsume), a pair
+  // starting on a measured state as a measuring pass -- instead of two single
+  // sweeps per check (each costs about a pass: 24 B per site for one update)
+  const bool fast = whole && t2_ok && s0->fast_checks && !(p->flags & PSG_RUN_EXACT);
+  auto norm_at = [&](int64_t t) { return p->norm_every > 0 && (p->step_offset + t) % p->norm_every == 0; };
   for (int64_t t = done_small ? p->steps + 1 : 1; t <= p->steps; ++t) {
+    if (fast && t + 1 <= p->steps && p->norm_every >= 2 && norm_at(t + 1) && !norm_at(t) &&
+        !meas_at(t) && !meas_at(t + 1) && !reimp_at(t) && s0->pending == s0->scal + S_ONE) {
+      { NvtxRange nv("psg:pass2_norm"); rc = do_sweep2_nrm(s0); }
+      if (rc) return rc;
+      ++t;
+      if (reimp_at(t)) {
+        for (int k = 0; k < p->n_impose && k < 3; ++k) {
+          rc = psg_impose(s0, p->impose_axis[k], p->impose_sign[k], 0);
+          if (rc) return rc;
+        }
+      }
+      continue;
+    }
+    if (fast && t + 1 <= p->steps && meas_at(t) && nc < want && !norm_at(t) && !norm_at(t + 1) &&
+        !meas_at(t + 1) && !reimp_at(t)) {
+      { NvtxRange nv("psg:pass2_measure"); rc = do_sweep2_ms(s0, s0->hist_dev + nc * rec); }
+      if (rc) return rc;
+      steps_of.push_back((double)(p->step_offset + t - 1));
+      ++nc;
+      ++t;
+      if (reimp_at(t)) {
+        for (int k = 0; k < p->n_impose && k < 3; ++k) {
+          rc = psg_impose(s0, p->impose_axis[k], p->impose_sign[k], 0);
+          if (rc) return rc;
+        }
+      }
+      continue;
+    }
     if (lin && t + 1 <= p->steps && p->norm_every > 0 &&
         (p->step_offset + t + 1) % p->norm_every == 0 && !meas_at(t) && !reimp_at(t) &&
         !meas_at(t + 1)) {

@@ -521,3 +521,40 @@ def test_device_inputs_match_host_recipes(gpu_lib, n, w, x_lo):
             kind, params = pot.device_generator(name, depth=-7.5)
             s.fill_potential(kind, params)
             assert np.array_equal(s.get_potential(), grid.v[x_lo - 1:x_lo + ww + 1]), name
+
+
+@pytest.mark.parametrize("n,steps,m,off,single", [(96, 61, 10, 0, False), (128, 83, 20, 7, False),
+                                                  (160, 45, 9, 3, False), (96, 50, 10, 0, True),
+                                                  (72, 40, 2, 1, False)])
+def test_checks_inside_two_sweep_passes(gpu_lib, n, steps, m, off, single):
+    """BASELINE fixed-step cadence (norm + observables every m) with the check
+    steps inside two-sweep passes (option 16): the pair ending on a
+    normalisation as a renormalising pass, the pair starting on a measured
+    state as a measuring pass (observables of its input in step 1, the
+    pending factor applied at the store).  Same records as the exact per-step
+    path, fields within 1e-13 max|psi|, plane sums within 1e-12; fewer launches."""
+    spec = LatticeSpec(N=n, a=0.3, m=1.0, dtau=0.3 * 0.3 / 4.0)
+    rng = np.random.default_rng(n + 5)
+    ext = n + 2
+    psi0 = np.zeros((ext,) * 3)
+    psi0[1:-1, 1:-1, 1:-1] = rng.uniform(-0.5, 0.5, (n, n, n))
+    v = np.zeros((ext,) * 3)
+    v[1:-1, 1:-1, 1:-1] = rng.uniform(-1.0, 3.0, (n, n, n))
+    outs = []
+    for exact in (True, False):
+        with Slab(spec, single_buffer=single, chunk=17 if single else 0) as s:
+            s.set_field(psi0)
+            s.set_potential(v)
+            l0 = s.launches()
+            idx, sums, st = s.run(steps, measure_every=m, norm_every=m, step_offset=off, exact=exact)
+            outs.append((s.get_field(), list(idx), np.asarray(sums), st, s.launches() - l0))
+    (f0, i0, s0, st0, l0), (f1, i1, s1, st1, l1) = outs
+    assert i1 == i0 and len(i0) > 0
+    assert not st0.any() and not st1.any()
+    assert np.abs(f1 - f0).max() <= 1e-13 * np.abs(f0).max()
+    np.testing.assert_allclose(s1, s0, rtol=1e-12, atol=1e-13 * np.abs(s0).max())
+    for a, b in zip(s0, s1):   # E and r_rms as evolve._record_from_sums forms them
+        assert abs(np.sum(b[0]) / np.sum(b[1]) - np.sum(a[0]) / np.sum(a[1])) <= 1e-12 * abs(
+            np.sum(a[0]) / np.sum(a[1]))
+    if m > 2:
+        assert l1 < l0
