@@ -348,10 +348,11 @@ typedef struct psg_run_params {
 #define PSG_RUN_LINEAR_NORM 1
 
 /* psg_run flag: exact.  Every norm / measure step through the per-step path
- * (plane sums over the sweep's tiles: bitwise the same run on any number of
- * slabs).  Without it, a small whole lattice (N <= 64, N % 16 == 0, no
- * re-imposition) runs its norm / measure steps inside the persistent brick
- * kernel (option 15), within roundoff (1e-13 max|psi|) of the per-step path. */
+ * (single sweeps; plane sums over the sweep's tiles: bitwise the same run on
+ * any number of slabs).  Without it, a whole-lattice slab runs its norm /
+ * measure steps inside the persistent brick kernel when N <= 64, N % 16 == 0
+ * and nothing is re-imposed (option 15), else inside two-sweep passes
+ * (option 16) -- within roundoff (1e-13 max|psi|) of the per-step path. */
 #define PSG_RUN_EXACT 2
 
 /* Fused fixed-step driver: runs the evolve_to_convergence loop body
@@ -430,7 +431,12 @@ int psg_tune(psg_slab* s, int blocks_per_sm, int zchunk, int stages);
  * pass; bitwise unchanged), 15 = the persistent brick kernel
  * also runs the norm / measure steps of a run inside the launch (whole run
  * without re-imposition in one launch; plane sums over bricks instead of
- * tiles: within roundoff of the per-step path, not bitwise; default 1). */
+ * tiles: within roundoff of the per-step path, not bitwise; default 1),
+ * 16 = whole-lattice runs take their norm / measure steps inside two-sweep
+ * passes: a pair ending on a normalisation as a renormalising pass, a pair
+ * starting on a measured state as a measuring pass (its input's observables
+ * in step 1, the pending factor applied at the store by linearity) -- within
+ * roundoff of the per-step path, not bitwise; default 1. */
 int psg_set_option(psg_slab* s, int option, int value);
 
 /* Enable / disable two sweeps per HBM pass (temporal blocking) for pairs of
