@@ -409,8 +409,9 @@ def evolve_fixed(initial: Field3D, grid: PotentialGrid, steps: int, measure_ever
     (psi, V), not three.  ``timings`` (extension): filled with the
     perf_counter seconds of the phases (upload, run, download).  ``exact``
     (extension): norm / measure steps through the per-step path (bitwise
-    evolve_parallel on any number of slabs); otherwise a small lattice (N <=
-    64) runs them inside its persistent brick kernel, within roundoff."""
+    evolve_parallel on any number of slabs); otherwise they run inside
+    two-sweep passes (a small lattice, N <= 64: inside its persistent brick
+    kernel), within roundoff."""
     import time
 
     from .device import Slab
