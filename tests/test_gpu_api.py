@@ -505,7 +505,7 @@ class TestSlabEngine:
         c = SymmetryConstraint("x", "antisymmetric")
         init = project(fill_random_gaussian(allocate(spec), 13), c)
         ref = evolve_fixed(init, grid, 90, 30, norm_every=30, constraints=[c],
-                           reimpose_every=30)
+                           reimpose_every=30, exact=True)
         par = evolve_parallel(grid, workers=workers, initial=init, check_freq=30, max_steps=90,
                               max_snapshots=0, norm_every=30, fixed=True, constraints=[c],
                               reimpose_freq=30)

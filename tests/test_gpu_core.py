@@ -64,7 +64,7 @@ def test_three_sweep_pass_matches_single_steps(gpu_lib, n, steps, every):
                 s.set_option(14, 1)
             s.set_field(psi0)
             s.set_potential(v)
-            idx, sums, status = s.run(steps, measure_every=every, norm_every=every)
+            idx, sums, status = s.run(steps, measure_every=every, norm_every=every, exact=True)
             out.append((s.get_field(), sums, s.launches()))
     assert np.array_equal(out[0][0], out[1][0])
     assert np.array_equal(out[0][1], out[1][1])
@@ -353,7 +353,7 @@ def test_two_step_pass_matches_single_steps(gpu_lib, n, steps, every, rows, stag
             s.set_t2_seg(seg)
             s.set_field(psi0)
             s.set_potential(v)
-            idx, sums, status = s.run(steps, measure_every=every, norm_every=every)
+            idx, sums, status = s.run(steps, measure_every=every, norm_every=every, exact=True)
             out.append((s.get_field(), sums, s.launches()))
     assert np.array_equal(out[0][0], out[1][0])
     assert np.array_equal(out[0][1], out[1][1])
@@ -390,7 +390,7 @@ def test_two_step_pass_coefficient_paths(gpu_lib, n, rows, wide, force, stages):
             s.set_t2_stages(stages)
             s.set_field(psi0)
             s.set_potential(v)
-            idx, sums, status = s.run(40, measure_every=20, norm_every=20)
+            idx, sums, status = s.run(40, measure_every=20, norm_every=20, exact=True)
             out.append((s.get_field(), sums))
     assert np.array_equal(out[0][0], out[1][0])
     assert np.array_equal(out[0][1], out[1][1])
@@ -450,7 +450,7 @@ def test_multi_slab_run_matches_whole_lattice(gpu_lib, n, widths, steps, every, 
         whole.set_temporal(t2)
         whole.set_field(psi0)
         whole.set_potential(v)
-        idx_w, sums_w, _ = whole.run(steps, measure_every=every, norm_every=every or 1)
+        idx_w, sums_w, _ = whole.run(steps, measure_every=every, norm_every=every or 1, exact=True)
         want = whole.get_field()
         meas_w = measure_multi([whole])
     slabs = []

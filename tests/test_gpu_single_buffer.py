@@ -35,8 +35,10 @@ def _run(spec, psi0, v, steps, every, single, chunk=0, t2=True, constraints=(), 
             s.set_option(o, val)
         s.set_field(psi0)
         s.set_potential(v)
+        # exact: norm / measure steps on the per-step path (these tests compare
+        # the pass implementations bit for bit across slab kinds and launches)
         idx, sums, status = s.run(steps, measure_every=every, norm_every=every,
-                                  reimpose_every=reimpose, constraints=constraints)
+                                  reimpose_every=reimpose, constraints=constraints, exact=True)
         return s.get_field(), np.asarray(sums), status, s.launches()
 
 
