@@ -1,0 +1,150 @@
+"""Randomised parity of the device engine against the CPU oracle.
+
+The parametrised tests elsewhere pin chosen geometries; this file draws them
+(hypothesis, derandomised so a failure reproduces): lattice sizes that leave
+partial tiles, bricks and z-chunks (odd, prime, one above / below a tile
+multiple), run lengths that end mid-pass, norm / measure / re-imposition
+cadences that cut two-sweep passes at every phase, single-buffer chunk
+sizes, potentials inside and outside the coefficients' fast range
+(d = 1 + (dtau/2) V outside [0.25, 4) takes the IEEE-division path), the
+exact and the default (checks inside passes) schedules, and 1-4 in-process
+slabs through the public evolve_parallel.
+
+Reference loop: evolve.py:249-270 (check on the state entering the sweep,
+sweep, renormalise, re-impose), restated below on the oracle's kernels.
+Bounds are north_star's: max|dpsi| <= 1e-12 max|psi|, E and r_rms within
+1e-10 relative; check steps must agree exactly."""
+
+import math
+
+import numpy as np
+import pytest
+from hypothesis import HealthCheck, given, settings
+from hypothesis import strategies as st
+
+from oracle import oracle as O
+from paper_0904_0939_b200.device import Slab
+from paper_0904_0939_b200.lattice import LatticeSpec
+
+pytestmark = pytest.mark.gpu
+
+FIELD_TOL = 1e-12
+OBS_TOL = 1e-10
+SIZES = [4, 5, 7, 8, 12, 15, 16, 17, 24, 31, 33, 40, 47, 48, 63, 64, 65, 72, 97, 128, 130, 161]
+FUZZ = settings(max_examples=200, deadline=None, derandomize=True, database=None,
+                suppress_health_check=[HealthCheck.too_slow,
+                                       HealthCheck.function_scoped_fixture])
+
+
+def _inputs(n, seed, vlo, vhi):
+    rng = np.random.default_rng(seed)
+    a = 0.3
+    spec = LatticeSpec(N=n, a=a, m=1.0, dtau=a * a / 4.0)
+    ext = n + 2
+    psi = np.zeros((ext,) * 3)
+    psi[1:-1, 1:-1, 1:-1] = rng.uniform(-0.5, 0.5, (n, n, n))
+    v = np.zeros((ext,) * 3)
+    v[1:-1, 1:-1, 1:-1] = rng.uniform(vlo, vhi, (n, n, n))
+    return spec, psi, v
+
+
+def oracle_run(spec, psi0, v, steps, measure_every, norm_every, reimpose_every, constraints):
+    """evolve.py:249-270 on the oracle's kernels, any number of constraints
+    applied in order (states.impose_inplace per constraint)."""
+    n, a, m, dtau = spec.N, spec.a, spec.m, spec.dtau
+    a3 = O.cell_volume(a)
+    psi, out = psi0.copy(), psi0.copy()
+    checks = []
+    for s in range(1, steps + 1):
+        if measure_every and s - 1 > 0 and (s - 1) % measure_every == 0:
+            e, _, r, *_ = O.observables(psi, v, n, a, m)
+            checks.append((s - 1, e, r))
+        O.stencil_update_v(psi, v, dtau, m, a, out, 1, n)
+        psi, out = out, psi
+        if norm_every and s % norm_every == 0:
+            n2 = O.np_sum(O.norm_plane_sums(psi, 1, n)) * a3
+            psi *= 1.0 / math.sqrt(n2)
+        if constraints and reimpose_every and s % reimpose_every == 0:
+            for axis, sign in constraints:
+                O.impose_copy(psi, n, axis, sign)
+    return psi, checks
+
+
+def _close(got, want):
+    return float(np.abs(got - want).max() / np.abs(want).max())
+
+
+CONSTRAINTS = [(), ((0, -1.0),), ((2, 1.0),), ((1, -1.0), (0, 1.0))]
+
+
+@FUZZ
+@given(n=st.sampled_from(SIZES), steps=st.integers(1, 90), me=st.integers(0, 25),
+       ne=st.integers(0, 25), exact=st.booleans(), single=st.booleans(),
+       chunk=st.integers(0, 9), wide=st.booleans(), cons=st.sampled_from(CONSTRAINTS),
+       re=st.integers(1, 30), linear=st.booleans(), seed=st.integers(0, 2 ** 16))
+def test_slab_run_matches_oracle(gpu_lib, n, steps, me, ne, exact, single, chunk, wide, cons,
+                                 re, linear, seed):
+    """psg_run on one whole-lattice slab (two-buffer or single-buffer) against
+    the oracle loop, every cadence and geometry drawn; ``linear``: pairs of
+    sweeps ending on a renormalisation as renormalising two-sweep passes
+    (evolve_to_convergence's default schedule)."""
+    # wide: V spans d = 1 + (dtau/2) V outside [0.25, 4) on some sites (the
+    # coefficients' IEEE-division path, no fast-path flag for the run)
+    spec, psi, v = _inputs(n, seed, *((-400.0, 400.0) if wide else (-1.0, 3.0)))
+    h = 0.5 * spec.dtau
+    if np.any(1.0 + h * v == 0.0):
+        return
+    if wide and not ne:
+        ne = 1   # unnormalised growth of up to 7x per sweep: keep it bounded
+    want, wchecks = oracle_run(spec, psi, v, steps, me, ne, re, cons)
+    with Slab(spec, single_buffer=single, chunk=chunk if single else 0) as s:
+        s.set_field(psi)
+        s.set_potential(v)
+        idx, sums, status = s.run(steps, measure_every=me, norm_every=ne,
+                                  reimpose_every=re if cons else 0, constraints=cons,
+                                  exact=exact, linear_norm=linear)
+        got = s.get_field()
+    assert not np.asarray(status).any()
+    err = _close(got, want)
+    assert err <= FIELD_TOL, f"max|dpsi|/max|psi| = {err:.3e}"
+    assert list(idx) == [c[0] for c in wchecks]
+    for (_, e, r), sm in zip(wchecks, sums):
+        den = float(np.sum(sm[1]))
+        ge = float(np.sum(sm[0])) / den
+        gr = math.sqrt(float(np.sum(sm[2])) / den)
+        assert abs(ge - e) <= OBS_TOL * abs(e), (ge, e)
+        assert abs(gr - r) <= OBS_TOL * abs(r), (gr, r)
+
+
+@FUZZ
+@given(shape=st.sampled_from([(8, 1), (8, 2), (12, 3), (16, 4), (20, 2), (33, 3), (40, 4),
+                              (48, 2), (64, 4), (66, 3)]),
+       steps=st.integers(2, 70), cf=st.integers(1, 20), ne=st.integers(1, 12),
+       cons=st.sampled_from(["", "x-", "z+", "y-x+"]), rf=st.integers(1, 25),
+       seed=st.integers(0, 2 ** 16))
+def test_evolve_parallel_matches_oracle(gpu_lib, shape, steps, cf, ne, cons, rf, seed):
+    """The public slab engine (evolve_parallel, in-process slabs on this GPU,
+    fixed-step mode) against the oracle loop: slab counts 1-4, constraints
+    across and along the slab axis, drawn cadences."""
+    from paper_0904_0939_b200 import PotentialGrid, SymmetryConstraint, evolve_parallel
+    from paper_0904_0939_b200.lattice import Field3D
+
+    n, workers = shape
+    spec, psi, v = _inputs(n, seed, -1.0, 3.0)
+    names = {"x": 0, "y": 1, "z": 2}
+    pairs, objs = [], []
+    for i in range(0, len(cons), 2):
+        ax, sg = cons[i], cons[i + 1]
+        pairs.append((names[ax], -1.0 if sg == "-" else 1.0))
+        objs.append(SymmetryConstraint(ax, "antisymmetric" if sg == "-" else "symmetric"))
+    want, wchecks = oracle_run(spec, psi, v, steps, cf, ne, rf, tuple(pairs))
+    grid = PotentialGrid(spec=spec, v=v, v_inf=0.0, unbounded=True, name="custom")
+    stt = evolve_parallel(grid, workers=workers, initial=Field3D(spec, psi.copy()),
+                          transport="inproc", check_freq=cf, max_steps=steps, max_snapshots=0,
+                          norm_every=ne, fixed=True, constraints=objs, reimpose_freq=rf)
+    err = _close(stt.psi.values, want)
+    assert err <= FIELD_TOL, f"max|dpsi|/max|psi| = {err:.3e}"
+    assert [c.step for c in stt.checks] == [c[0] for c in wchecks]
+    for c, (_, e, r) in zip(stt.checks, wchecks):
+        assert abs(c.energy - e) <= OBS_TOL * abs(e)
+        assert abs(c.r_rms - r) <= OBS_TOL * abs(r)
