@@ -148,3 +148,105 @@ def test_evolve_parallel_matches_oracle(gpu_lib, shape, steps, cf, ne, cons, rf,
     for c, (_, e, r) in zip(stt.checks, wchecks):
         assert abs(c.energy - e) <= OBS_TOL * abs(e)
         assert abs(c.r_rms - r) <= OBS_TOL * abs(r)
+
+
+@FUZZ
+@given(n=st.sampled_from(SIZES[:19]), data=st.data(), seed=st.integers(0, 2 ** 16))
+def test_operator_layer_matches_oracle(gpu_lib, n, data, seed):
+    """The C-ABI operator layer (psg_kernel_*, the ctypes body of
+    psibox.kernels) on slab-shaped arrays (W+2, N+2, N+2) with a drawn plane
+    range: the updates bitwise, outside the range and the padding untouched;
+    the plane sums within 1e-13 of the oracle's sequential sums per plane."""
+    from paper_0904_0939_b200 import kernels as K
+
+    w = data.draw(st.integers(1, n))
+    x_lo = data.draw(st.integers(1, w))
+    x_hi = data.draw(st.integers(x_lo, w))
+    rng = np.random.default_rng(seed)
+    shape = (w + 2, n + 2, n + 2)
+    psi = rng.standard_normal(shape)
+    v = rng.uniform(-2.0, 6.0, shape)
+    a, m = 0.4, 1.7
+    dtau = a * a / 4.0
+    want = rng.standard_normal(shape)
+    got = want.copy()
+    O.stencil_update_v(psi, v, dtau, m, a, want, x_lo, x_hi)
+    K.stencil_update_v(psi, v, dtau, m, a, got, x_lo, x_hi)
+    assert np.array_equal(got, want)
+    ca, cc = rng.uniform(0.5, 1.0, shape), rng.uniform(0.0, 0.2, shape)
+    O.stencil_update(psi, ca, cc, want, x_lo, x_hi)
+    K.stencil_update(psi, ca, cc, got, x_lo, x_hi)
+    assert np.array_equal(got, want)
+
+    def near(g, o):
+        assert np.all(np.abs(g - o) <= 1e-13 * np.abs(o) + 1e-300), (g, o)
+
+    k = x_hi - x_lo + 1
+    out = np.empty(k)
+    K.norm_plane_sums(psi, x_lo, x_hi, out)
+    near(out, O.norm_plane_sums(psi, x_lo, x_hi))
+    num, den = np.empty(k), np.empty(k)
+    kin = 1.0 / (2.0 * m * a * a)
+    K.energy_plane_sums(psi, v, kin, x_lo, x_hi, num, den)
+    onum, oden = O.energy_plane_sums(psi, v, kin, x_lo, x_hi)
+    # num sums terms of both signs: its error is relative to the sum of |terms|
+    scale = O.energy_plane_sums(np.abs(psi), np.abs(v), -abs(kin), x_lo, x_hi)[0]
+    assert np.all(np.abs(num - onum) <= 1e-13 * np.abs(scale)), (num, onum)
+    near(den, oden)
+    x0 = data.draw(st.integers(1, n - w + 1))
+    r2, den2 = np.empty(k), np.empty(k)
+    K.radius2_plane_sums(psi, x0, 0.5 * (n + 1), a, x_lo, x_hi, r2, den2)
+    or2, oden2 = O.radius2_plane_sums(psi, x0, 0.5 * (n + 1), a, x_lo, x_hi)
+    near(r2, or2)
+    near(den2, oden2)
+    dot = np.empty(k)
+    psi2 = np.abs(rng.standard_normal(shape))
+    K.dot_plane_sums(np.abs(psi), psi2, x_lo, x_hi, dot)
+    near(dot, O.dot_plane_sums(np.abs(psi), psi2, x_lo, x_hi))
+
+
+@FUZZ
+@given(n=st.sampled_from(SIZES), axis=st.integers(0, 2), sign=st.sampled_from([-1.0, 1.0]),
+       projector=st.booleans(), seed=st.integers(0, 2 ** 16))
+def test_impose_and_project_match_oracle(gpu_lib, n, axis, sign, projector, seed):
+    """states.impose_inplace (copy semantics, odd N's centre plane) and the
+    parity projector on every storage axis: bitwise the oracle."""
+    from paper_0904_0939_b200.lattice import Field3D
+    from paper_0904_0939_b200.states import SymmetryConstraint, impose_inplace, project
+
+    rng = np.random.default_rng(seed)
+    spec = LatticeSpec(N=n, a=0.5, m=1.0, dtau=0.0625)
+    vals = np.zeros((n + 2,) * 3)
+    vals[1:-1, 1:-1, 1:-1] = rng.standard_normal((n, n, n))
+    c = SymmetryConstraint("xyz"[axis], "antisymmetric" if sign < 0 else "symmetric")
+    if projector:
+        got = project(Field3D(spec, vals.copy()), c).values
+        want = O.project(vals, axis, sign)
+    else:
+        got = impose_inplace(vals.copy(), n, c)
+        want = O.impose_copy(vals.copy(), n, axis, sign)
+    assert np.array_equal(got, want)
+
+
+@FUZZ
+@given(pair=st.sampled_from([(8, 16), (16, 32), (12, 24), (10, 15), (9, 27), (20, 30),
+                             (32, 48), (30, 60), (24, 40), (16, 12), (33, 22), (64, 128)]),
+       seed=st.integers(0, 2 ** 16))
+def test_resample_matches_oracle(gpu_lib, pair, seed):
+    """multires.resample between lattices of one box side (finer, coarser,
+    non-integer ratios): the oracle's nested lerps renormalised, 1e-14."""
+    from paper_0904_0939_b200.lattice import Field3D
+    from paper_0904_0939_b200.multires import resample
+
+    nc, nf = pair
+    box = 6.0
+    cs = LatticeSpec(N=nc, a=box / nc, m=1.0, dtau=(box / nc) ** 2 / 4.0)
+    fs = LatticeSpec(N=nf, a=box / nf, m=1.0, dtau=(box / nf) ** 2 / 4.0)
+    rng = np.random.default_rng(seed)
+    vals = np.zeros((nc + 2,) * 3)
+    vals[1:-1, 1:-1, 1:-1] = rng.uniform(-0.5, 0.5, (nc,) * 3)
+    got = resample(Field3D(cs, vals), fs).values
+    want = O.resample(vals, nc, cs.a, nf, fs.a)
+    n2 = O.np_sum(O.norm_plane_sums(want, 1, nf)) * O.cell_volume(fs.a)
+    want *= 1.0 / math.sqrt(n2)
+    assert _close(got, want) <= 1e-14
