@@ -594,7 +594,7 @@ def run_single_gpu(args):
     slab.sync()
 
     # ---- timed region: K sweeps (observables + renormalisation every m), reps ----
-    times, launches, e_last = [], None, None
+    times, launches, e_last, nchecks = [], None, None, 0
     offset = args.warmup
     with ClockSampler(dev) as clk:
         for r in range(args.reps):
@@ -612,6 +612,7 @@ def run_single_gpu(args):
             times.append(e0.elapsed_time(e1))
             if launches is None:
                 launches = slab.launches() - l0
+            nchecks += len(sums)
             if len(sums):
                 e_last = float(np.sum(sums[-1][0]) / np.sum(sums[-1][1]))
             offset += args.steps
@@ -672,7 +673,9 @@ def run_single_gpu(args):
         "e2e": e2e,
         "gpu_launches": launches,
         "cpu_baseline": cpu,
-        "observables": {"E_last": e_last},
+        # E of the last check inside the timed regions (none when K < m: the
+        # e2e job's checks are in e2e.E_last)
+        "observables": {"E_last": e_last, "checks_in_timed_regions": nchecks},
     }
     if e2e is None:
         line["e2e_note"] = e2e_note
