@@ -21,6 +21,10 @@ test_gpu_api.py::TestGolden::test_config1_end_to_end.  Here:
   C5  the wells recipe (harmonic + 8 Gaussian wells, box side 20) at 256^3,
       2000 sweeps, observables + norm every 100
 
+PSG_KSTEP_FULL=1 runs C3 at its full BASELINE length (40000 sweeps, observables
++ norm and re-imposition every 1000; ~25 min of the oracle on 16 threads) and
+the C5 recipe at 512^3; the default suite keeps the reduced ones.
+
 Reduction order (why the tolerance is not bitwise): every sweep, coefficient,
 imposition and resample lerp is bitwise the oracle's; plane sums are
 tree-ordered on the device where the oracle sums sequentially,
@@ -30,6 +34,7 @@ The measured differences are printed (pytest -s) and recorded in DESIGN.md.
 """
 
 import math
+import os
 
 import numpy as np
 import pytest
@@ -94,7 +99,8 @@ def test_c2_full_20000_sweeps(gpu_lib):
 def test_c3_projector_start_512(gpu_lib):
     w = workloads.CONFIGS["C3"]
     spec = w.spec
-    steps, m, reimp = 2000, 500, 1000
+    full = os.environ.get("PSG_KSTEP_FULL") == "1"
+    steps, m, reimp = (w.steps, w.measure_every, 1000) if full else (2000, 500, 1000)
     init = workloads.uniform_field(spec)
     grid = workloads.make_grid(w, spec)
     c = SymmetryConstraint("x", "antisymmetric")    # storage axis 0 (BASELINE's z)
@@ -105,7 +111,8 @@ def test_c3_projector_start_512(gpu_lib):
                       reimpose_every=reimp)
     psi_want, checks_want = _oracle_run(start_want, grid, spec, steps, m, reimpose_every=reimp,
                                         impose_axis=0, impose_sign=-1.0)
-    _compare("C3 512^3 x 2000 (projector start, re-impose / 1000)", st, psi_want, checks_want)
+    _compare(f"C3 512^3 x {steps} (projector start, checks / {m}, re-impose / {reimp})", st,
+             psi_want, checks_want)
     # both ends are exactly odd after the last re-imposition
     assert np.array_equal(st.psi.values, -st.psi.values[::-1])
     _final_observables(st, grid, spec, psi_want)
@@ -139,12 +146,13 @@ def test_c4_cornell_ladder(gpu_lib):
 
 
 def test_c5_recipe_256(gpu_lib):
-    w = workloads.scaled(workloads.CONFIGS["C5"], 256, steps=2000)
+    n = 512 if os.environ.get("PSG_KSTEP_FULL") == "1" else 256
+    w = workloads.scaled(workloads.CONFIGS["C5"], n, steps=2000)
     spec = w.spec
     init = workloads.uniform_field(spec)
     grid = workloads.make_grid(w, spec)
     m = w.measure_every
     st = evolve_fixed(init, grid, w.steps, m, norm_every=m)
     psi_want, checks_want = _oracle_run(init.values, grid, spec, w.steps, m)
-    _compare("C5 recipe 256^3 x 2000", st, psi_want, checks_want)
+    _compare(f"C5 recipe {n}^3 x 2000", st, psi_want, checks_want)
     _final_observables(st, grid, spec, psi_want)
