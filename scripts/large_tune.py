@@ -1,6 +1,9 @@
 """Two-sweep pass time at large N vs chunk / z-chunk / work split (developer tool).
 
-    python scripts/large_tune.py [N] [--chunks 0,128,256,512] [--zcs 0,32,64,128] [--segs 0,1,2]
+    python scripts/large_tune.py [N] [--chunks 0,128,256,512] [--zcs 0,32,64,128] [--segs 0,1,2] [--lib PATH]
+
+Compare settings in SEPARATE processes, alternating: the first setting timed in a process
+runs before the board reaches its power cap and looks 1-3 % faster than it is.
 
 Single-buffer slab with device-generated C5 inputs; prints one JSON line per
 setting: mean pass time over `reps` back-to-back passes and the GB/s of the
@@ -28,7 +31,10 @@ def main():
     ap.add_argument("--segs", default="0")
     ap.add_argument("--reps", type=int, default=8)
     ap.add_argument("--single", type=int, default=1)
+    ap.add_argument("--lib", default="", help="library to load instead of the tree's (scripts/ab builds)")
     a = ap.parse_args()
+    if a.lib:
+        _lib.LIB_PATH = a.lib
     w = workloads.scaled(workloads.CONFIGS["C5"], a.n)
     n = w.spec.N
     for chunk in [int(x) for x in a.chunks.split(",")]:
@@ -49,7 +55,7 @@ def main():
                 e1.record(st)
                 e1.synchronize()
                 t = e0.elapsed_time(e1) * 1e-3 / a.reps
-                print(json.dumps({"n": n, "chunk": chunk, "zc": zc, "seg": seg,
+                print(json.dumps({"n": n, "lib": os.path.basename(a.lib) or "tree", "chunk": chunk, "zc": zc, "seg": seg,
                                   "pass_ms": t * 1e3, "GBps": 24 * n ** 3 / t / 1e9,
                                   "launches_per_pass": (s.launches() - l0) / a.reps}), flush=True)
         s.close()
