@@ -31,6 +31,8 @@ def main():
     ap.add_argument("--segs", default="0")
     ap.add_argument("--reps", type=int, default=8)
     ap.add_argument("--single", type=int, default=1)
+    ap.add_argument("--set", default="", help="Slab setters to call first: method=value[,method=value]")
+    ap.add_argument("--reserve", type=int, default=-1, help="time psg_pass with this many SMs left idle instead of psg_run")
     ap.add_argument("--lib", default="", help="library to load instead of the tree's (scripts/ab builds)")
     a = ap.parse_args()
     if a.lib:
@@ -41,6 +43,9 @@ def main():
         _lib.load().psg_trim_memory(0)
         s = Slab(w.spec, single_buffer=bool(a.single), chunk=chunk)
         workloads.fill_slab(s, w)
+        for kv in filter(None, a.set.split(",")):
+            k, v = kv.split("=")
+            getattr(s, k)(int(v))
         st = torch.cuda.ExternalStream(s.stream)
         for zc in [int(x) for x in a.zcs.split(",")]:
             for seg in [int(x) for x in a.segs.split(",")]:
@@ -51,11 +56,15 @@ def main():
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 l0 = s.launches()
                 e0.record(st)
-                s.run(2 * a.reps, 0, 0)
+                if a.reserve >= 0:
+                    for _ in range(a.reps):
+                        s.pass2(a.reserve)
+                else:
+                    s.run(2 * a.reps, 0, 0)
                 e1.record(st)
                 e1.synchronize()
                 t = e0.elapsed_time(e1) * 1e-3 / a.reps
-                print(json.dumps({"n": n, "lib": os.path.basename(a.lib) or "tree", "chunk": chunk, "zc": zc, "seg": seg,
+                print(json.dumps({"n": n, "lib": os.path.basename(a.lib) or "tree", "set": a.set, "reserve": a.reserve, "chunk": chunk, "zc": zc, "seg": seg,
                                   "pass_ms": t * 1e3, "GBps": 24 * n ** 3 / t / 1e9,
                                   "launches_per_pass": (s.launches() - l0) / a.reps}), flush=True)
         s.close()
