@@ -413,7 +413,8 @@ int psg_tune(psg_slab* s, int blocks_per_sm, int zchunk, int stages);
  * its predecessor wrote last, still in L2 (default 1; bitwise unchanged),
  * 3 = tile rows of the two-sweep pass, 8 (two blocks per SM) or 16 (one
  * block per SM, default; bitwise unchanged), 4 = always take the range-checked
- * coefficient path, 5 = TMA stages of the 16-row two-sweep pass (6 or 9),
+ * coefficient path, 5 = TMA stages of the 16-row two-sweep pass (0 = automatic,
+ * the default: 7 for 192 <= N <= 640, else 6; or 6, 7, 9; bitwise unchanged),
  * 6 = two-sweep passes alternate their chunk order (default 1),
  * 8 = work split of the two-sweep pass: 0 automatic (default), 1 round-robin
  * chunk items, 2 one contiguous (tile, plane) range per block (bitwise

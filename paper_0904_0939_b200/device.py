@@ -181,7 +181,7 @@ class Slab:
         self.set_option(2, value)
 
     def set_t2_stages(self, stages: int):
-        """TMA pipeline depth of the 16-row two-sweep pass: 6 or 9."""
+        """TMA pipeline depth of the 16-row two-sweep pass: 0 (automatic), 6, 7 or 9."""
         self.set_option(5, stages)
 
     def set_t2_alt(self, on: int):

@@ -332,7 +332,7 @@ def test_coefficient_division_is_ieee(gpu_lib, lo, hi):
 @pytest.mark.parametrize("n,steps,every", [(8, 9, 0), (16, 50, 0), (40, 123, 20), (64, 300, 100),
                                            (100, 61, 0), (130, 64, 30), (256, 20, 10)])
 @pytest.mark.parametrize("rows,stages,seg", [(8, 6, 1), (16, 6, 1), (16, 9, 1), (16, 6, 2),
-                                             (16, 6, 0)])
+                                             (16, 6, 0), (16, 7, 0), (16, 0, 0)])
 def test_two_step_pass_matches_single_steps(gpu_lib, n, steps, every, rows, stages, seg):
     """Temporal blocking (two sweeps per HBM pass, intermediate plane ring in
     shared memory) gives the same bits as one launch per sweep."""
@@ -363,7 +363,7 @@ def test_two_step_pass_matches_single_steps(gpu_lib, n, steps, every, rows, stag
 
 @pytest.mark.parametrize("n,rows,wide,force", [(40, 16, False, True), (72, 16, True, False),
                                                (72, 8, True, False), (130, 16, True, True)])
-@pytest.mark.parametrize("stages", [6, 9])
+@pytest.mark.parametrize("stages", [6, 7, 9])
 def test_two_step_pass_coefficient_paths(gpu_lib, n, rows, wide, force, stages):
     """The two-step pass's coefficient paths: without the per-plane range vote
     (every d = 1 + hV in [0.25, 4), checked at upload), with it (option 4),
